@@ -1,0 +1,432 @@
+// all_reduce over NVLink peer memory: one-shot (K1), two-shot (K2) and the
+// fused pack -> reduce -> unpack variant (K9).
+//
+// Reference algorithms being replaced (collectives.py):
+//   _allreduce_naive   :296-312  gather to rank 0, fold ascending, send back
+//   _allreduce_ring    :355-382  ring RS + AG over even_segments (:163-171)
+//   FusionManager flush (middleware.py:311-344) concat -> all_reduce -> scatter
+// Both kernels here fold the p contributions in ASCENDING rank order with a
+// single pass per element, exactly the sequential oracle's fold
+// (reference.py:16-20, tests/seqref.py:13-24), so f32/f64 results are
+// bit-identical to the oracle (bf16: f32 accumulation, one RNE rounding).
+#include "internal.h"
+
+namespace mcrdl {
+
+// ----------------------------------------------------------------- one-shot
+// Block b owns packs [pb, pe) of the message. Phase 1 pushes them into every
+// peer's workspace slot `rank`; phase 2 folds slots 0..p-1 (own input for
+// slot == rank) into `out`. Latency: one NVLink write + one flag per peer.
+template <typename T, int OP, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    k_ar_oneshot(DevComm c, const T* in, T* out, int64_t n, int64_t slot_bytes, uint32_t epoch,
+                 uint32_t sig) {
+  constexpr int N = Pack<T>::N;
+  __shared__ int s_err;
+  __shared__ SComm S;
+  const int par = epoch & 1, rank = c.rank, world = c.world;
+  const int b = blockIdx.x, G = gridDim.x, tid = threadIdx.x, nt = blockDim.x;
+  const int64_t npk = (n + N - 1) / N;
+  const int64_t pb = npk * b / G, pe = npk * (b + 1) / G;
+  const int64_t hoff = int64_t(par) * c.half_bytes;
+  if (tid == 0) s_err = 0;
+  stage_comm(c, S);
+  __syncthreads();
+
+  // Phase 1: each pack read once from HBM, written to p-1 peers.
+  for (int64_t i = pb + tid; i < pe; i += nt) {
+    const uint4 v = load_pack<T, VEC>(in, i, n);
+    for (int k = 1; k < world; ++k) {
+      const int q = (rank + k) % world;
+      st16(S.ws[q] + hoff + int64_t(rank) * slot_bytes + i * 16, v);
+    }
+  }
+  __syncthreads();
+  const uint64_t f = make_flag(epoch, sig, 0);
+  if (tid < world && tid != rank) publish(&S.pad[tid]->flag[par][b][rank], f);
+  if (tid < world && tid != rank) {
+    int e = wait_flag(&S.pad[rank]->flag[par][b][tid], S.pad[rank], c.timeout_ns, epoch, sig, 0);
+    if (e) atomicCAS(&s_err, 0, e);
+  }
+  __syncthreads();
+  if (s_err) {
+    if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+    return;
+  }
+  // Phase 2: ascending fold.
+  const uint8_t* ws = S.ws[rank] + hoff;
+  for (int64_t i = pb + tid; i < pe; i += nt) {
+    Pack<T> acc;
+    acc.from_raw(rank == 0 ? load_pack<T, VEC>(in, i, n) : ld16_cg(ws + i * 16));
+    for (int r = 1; r < world; ++r) {
+      const uint4 v = (r == rank) ? load_pack<T, VEC>(in, i, n)
+                                  : ld16_cg(ws + int64_t(r) * slot_bytes + i * 16);
+      acc.template fold<OP>(v);
+    }
+    store_pack<T, VEC>(out, i, n, acc.to_raw());
+  }
+}
+
+// ----------------------------------------------------------------- two-shot
+// Segment j = packs [j*sp, (j+1)*sp) (sp = ceil(npk / p)); block b owns the
+// same sub-range [b*sp/G, (b+1)*sp/G) of every segment.
+//   RS: push my copy of segment j to rank j (RS area, slot `rank`); flag.
+//   fold: segment `rank` = ascending fold of the p slots -> out + every
+//         peer's AG area (slot `rank`); flag2.
+//   AG: copy AG slots r != rank into out.
+// Workspace per half: RS area p*segb + AG area p*segb.
+template <typename T, int OP, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    k_ar_twoshot(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb,
+                 uint32_t epoch, uint32_t sig) {
+  constexpr int N = Pack<T>::N;
+  __shared__ int s_err;
+  __shared__ SComm S;
+  const int par = epoch & 1, rank = c.rank, world = c.world;
+  const int b = blockIdx.x, G = gridDim.x, tid = threadIdx.x, nt = blockDim.x;
+  const int64_t npk = (n + N - 1) / N;
+  const int64_t rb = sp * b / G, re = sp * (b + 1) / G;  // sub-range within a segment
+  const int64_t hoff = int64_t(par) * c.half_bytes;
+  const int64_t ag = int64_t(world) * segb;
+  if (tid == 0) s_err = 0;
+  stage_comm(c, S);
+  __syncthreads();
+
+  // ---- RS push: for each sub-range pack, send segment j's copy to rank j.
+  for (int64_t i = rb + tid; i < re; i += nt) {
+    for (int k = 1; k < world; ++k) {
+      const int q = (rank + k) % world;
+      const int64_t gi = int64_t(q) * sp + i;
+      if (gi >= npk) continue;
+      const uint4 v = load_pack<T, VEC>(in, gi, n);
+      st16(S.ws[q] + hoff + int64_t(rank) * segb + i * 16, v);
+    }
+  }
+  __syncthreads();
+  if (tid < world && tid != rank) publish(&S.pad[tid]->flag[par][b][rank], make_flag(epoch, sig, 0));
+  if (tid < world && tid != rank) {
+    int e = wait_flag(&S.pad[rank]->flag[par][b][tid], S.pad[rank], c.timeout_ns, epoch, sig, 0);
+    if (e) atomicCAS(&s_err, 0, e);
+  }
+  __syncthreads();
+  if (s_err) {
+    if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+    return;
+  }
+
+  // ---- fold my segment, scatter the result to every peer's AG area.
+  const uint8_t* ws = S.ws[rank] + hoff;
+  for (int64_t i = rb + tid; i < re; i += nt) {
+    const int64_t gi = int64_t(rank) * sp + i;
+    if (gi >= npk) break;
+    Pack<T> acc;
+    acc.from_raw(rank == 0 ? load_pack<T, VEC>(in, gi, n) : ld16_cg(ws + i * 16));
+    for (int r = 1; r < world; ++r) {
+      const uint4 v = (r == rank) ? load_pack<T, VEC>(in, gi, n)
+                                  : ld16_cg(ws + int64_t(r) * segb + i * 16);
+      acc.template fold<OP>(v);
+    }
+    const uint4 res = acc.to_raw();
+    for (int k = 1; k < world; ++k) {
+      const int q = (rank + k) % world;
+      st16(S.ws[q] + hoff + ag + int64_t(rank) * segb + i * 16, res);
+    }
+    store_pack<T, VEC>(out, gi, n, res);
+  }
+  __syncthreads();
+  if (tid < world && tid != rank) publish(&S.pad[tid]->flag2[par][b][rank], make_flag(epoch, sig, 1));
+  if (tid < world && tid != rank) {
+    int e = wait_flag(&S.pad[rank]->flag2[par][b][tid], S.pad[rank], c.timeout_ns, epoch, sig, 1);
+    if (e) atomicCAS(&s_err, 0, e);
+  }
+  __syncthreads();
+  if (s_err) {
+    if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+    return;
+  }
+
+  // ---- AG: land every other rank's reduced segment in `out`.
+  for (int64_t i = rb + tid; i < re; i += nt) {
+    for (int k = 1; k < world; ++k) {
+      const int r = (rank + k) % world;
+      const int64_t gi = int64_t(r) * sp + i;
+      if (gi >= npk) continue;
+      store_pack<T, VEC>(out, gi, n, ld16_cg(ws + ag + int64_t(r) * segb + i * 16));
+    }
+  }
+}
+
+// ------------------------------------------------------------- fused (K9)
+// Members laid out back to back in a virtual packed buffer (element offsets
+// d_off[m], 16-byte aligned). One-shot protocol over the packed index space:
+// phase 1 packs member inputs straight into every peer's workspace; phase 2
+// folds and unpacks straight into member outputs. No staging buffer, one
+// launch (reference: np.concatenate + all_reduce + _scatter_back,
+// middleware.py:316-341).
+template <typename T, int OP>
+__global__ void __launch_bounds__(kThreads)
+    k_ar_fused(DevComm c, const T* const* in_ptrs, T* const* out_ptrs, const int64_t* counts,
+               const int64_t* offs, int nmem, int64_t total, int64_t slot_bytes, uint32_t epoch,
+               uint32_t sig) {
+  constexpr int N = Pack<T>::N;
+  __shared__ int s_err;
+  __shared__ SComm S;
+  __shared__ int s_m0;
+  const int par = epoch & 1, rank = c.rank, world = c.world;
+  const int b = blockIdx.x, G = gridDim.x, tid = threadIdx.x, nt = blockDim.x;
+  const int64_t npk = (total + N - 1) / N;
+  const int64_t pb = npk * b / G, pe = npk * (b + 1) / G;
+  const int64_t hoff = int64_t(par) * c.half_bytes;
+  if (tid == 0) {
+    s_err = 0;
+    // first member whose packed range ends after pb
+    int lo = 0, hi = nmem;
+    while (lo < hi) {
+      int mid = (lo + hi) / 2;
+      if ((offs[mid] + counts[mid] + N - 1) / N <= pb) lo = mid + 1;
+      else hi = mid;
+    }
+    s_m0 = lo;
+  }
+  stage_comm(c, S);
+  __syncthreads();
+  const int m0 = s_m0;
+
+  for (int m = m0; m < nmem; ++m) {
+    const int64_t mp0 = offs[m] / N;                      // member's first pack
+    const int64_t mpn = (counts[m] + N - 1) / N;          // member packs
+    if (mp0 >= pe) break;
+    const int64_t a = max(pb, mp0), z = min(pe, mp0 + mpn);
+    const T* src = in_ptrs[m];
+    const bool vec = (uintptr_t(src) & 15) == 0;
+    for (int64_t i = a + tid; i < z; i += nt) {
+      const uint4 v = vec ? load_pack<T, true>(src, i - mp0, counts[m])
+                          : load_pack<T, false>(src, i - mp0, counts[m]);
+      for (int k = 1; k < world; ++k) {
+        const int q = (rank + k) % world;
+        st16(S.ws[q] + hoff + int64_t(rank) * slot_bytes + i * 16, v);
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < world && tid != rank) publish(&S.pad[tid]->flag[par][b][rank], make_flag(epoch, sig, 0));
+  if (tid < world && tid != rank) {
+    int e = wait_flag(&S.pad[rank]->flag[par][b][tid], S.pad[rank], c.timeout_ns, epoch, sig, 0);
+    if (e) atomicCAS(&s_err, 0, e);
+  }
+  __syncthreads();
+  if (s_err) {
+    if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+    return;
+  }
+  const uint8_t* ws = S.ws[rank] + hoff;
+  for (int m = m0; m < nmem; ++m) {
+    const int64_t mp0 = offs[m] / N;
+    const int64_t mpn = (counts[m] + N - 1) / N;
+    if (mp0 >= pe) break;
+    const int64_t a = max(pb, mp0), z = min(pe, mp0 + mpn);
+    const T* src = in_ptrs[m];
+    T* dst = out_ptrs[m];
+    const int64_t cnt = counts[m];
+    const bool vec = ((uintptr_t(src) | uintptr_t(dst)) & 15) == 0;
+    for (int64_t i = a + tid; i < z; i += nt) {
+      const int64_t li = i - mp0;
+      Pack<T> acc;
+      auto own = [&]() {
+        return vec ? load_pack<T, true>(src, li, cnt) : load_pack<T, false>(src, li, cnt);
+      };
+      acc.from_raw(rank == 0 ? own() : ld16_cg(ws + i * 16));
+      for (int r = 1; r < world; ++r) {
+        const uint4 v = (r == rank) ? own() : ld16_cg(ws + int64_t(r) * slot_bytes + i * 16);
+        acc.template fold<OP>(v);
+      }
+      if (vec) store_pack<T, true>(dst, li, cnt, acc.to_raw());
+      else store_pack<T, false>(dst, li, cnt, acc.to_raw());
+    }
+  }
+}
+
+// Local copy used for world == 1 (the p = 1 floor: out[:] = in).
+__global__ void __launch_bounds__(kThreads) k_copy(uint8_t* dst, const uint8_t* src, int64_t n) {
+  int64_t s, e;
+  byte_share(n, blockIdx.x, gridDim.x, s, e);
+  block_copy<4>(dst + s, src + s, e - s);
+}
+
+// ----------------------------------------------------------------- launch
+static int grid_for(int64_t packs, int num_sms, int max_blocks) {
+  // ~2 packs per thread per block for small messages, up to 2 CTAs per SM.
+  int64_t g = (packs + int64_t(kThreads) * 2 - 1) / (int64_t(kThreads) * 2);
+  int cap = max_blocks;
+  if (cap > 2 * num_sms) cap = 2 * num_sms;
+  if (cap > kMaxBlocks) cap = kMaxBlocks;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return int(g);
+}
+
+mcrdl_status_t launch_local_copy(void* dst, const void* src, int64_t nbytes, int num_sms,
+                                 cudaStream_t stream) {
+  if (nbytes <= 0 || dst == src) return MCRDL_OK;
+  int64_t g = (nbytes + (int64_t(kThreads) * 64) - 1) / (int64_t(kThreads) * 64);
+  if (g > 4 * num_sms) g = 4 * num_sms;
+  if (g < 1) g = 1;
+  k_copy<<<int(g), kThreads, 0, stream>>>(reinterpret_cast<uint8_t*>(dst),
+                                          reinterpret_cast<const uint8_t*>(src), nbytes);
+  count_launch();
+  MCRDL_CUDA_CHECK(cudaGetLastError());
+  return MCRDL_OK;
+}
+
+template <typename T, int OP>
+static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mcrdl_algo_t algo,
+                               uint64_t seq, int dt, cudaStream_t stream) {
+  constexpr int N = Pack<T>::N;
+  const int world = c->world;
+  const int64_t half = c->dc.half_bytes;
+  const bool vec = ((uintptr_t(in) | uintptr_t(out)) & 15) == 0;
+  if (world == 1) return launch_local_copy(out, in, n * int64_t(sizeof(T)), c->num_sms, stream);
+  const int64_t bytes = n * int64_t(sizeof(T));
+  const int64_t oneshot_max = half / world / 256 * 256;
+  if (algo == MCRDL_ALGO_AUTO) algo = (bytes <= (int64_t(512) << 10)) ? MCRDL_ALGO_ONE_SHOT : MCRDL_ALGO_TWO_SHOT;
+  if (algo == MCRDL_ALGO_NVLS) algo = MCRDL_ALGO_TWO_SHOT;  // TODO(nvls): multicast path
+  if (algo == MCRDL_ALGO_ONE_SHOT && bytes > oneshot_max) algo = MCRDL_ALGO_TWO_SHOT;
+
+  // Host chunking keeps every launch inside one workspace half.
+  const int64_t chunk_elems = (algo == MCRDL_ALGO_ONE_SHOT)
+                                  ? n
+                                  : ((half / 2 - int64_t(world) * 1024) / int64_t(sizeof(T))) /
+                                        (int64_t(world) * 4 * N) * (int64_t(world) * 4 * N);
+  int64_t done = 0;
+  int sub = 0;
+  do {
+    const int64_t m = (n - done < chunk_elems) ? (n - done) : chunk_elems;
+    uint32_t epoch;
+    mcrdl_status_t st = begin_op(c, &epoch);
+    if (st != MCRDL_OK) return st;
+    const uint32_t sig = op_sig(kKindAllReduce, dt, OP, sub, uint64_t(m), seq);
+    const T* ip = in + done;
+    T* op = out + done;
+    const int64_t npk = (m + N - 1) / N;
+    if (algo == MCRDL_ALGO_ONE_SHOT) {
+      const int64_t slot = (npk * 16 + 255) / 256 * 256;
+      const int G = grid_for(npk, c->num_sms, 64);
+      if (vec)
+        k_ar_oneshot<T, OP, true><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, slot, epoch, sig);
+      else
+        k_ar_oneshot<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, slot, epoch, sig);
+    } else {
+      const int64_t sp = (npk + world - 1) / world;
+      const int64_t segb = (sp * 16 + 255) / 256 * 256;
+      const int G = grid_for(sp, c->num_sms, 2 * c->num_sms);
+      if (vec)
+        k_ar_twoshot<T, OP, true><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, epoch, sig);
+      else
+        k_ar_twoshot<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, epoch, sig);
+    }
+    count_launch();
+    MCRDL_CUDA_CHECK(cudaGetLastError());
+    done += m;
+    ++sub;
+  } while (done < n);
+  return MCRDL_OK;
+}
+
+template <typename T>
+static mcrdl_status_t ar_op(mcrdl_comm* c, const void* in, void* out, int64_t n, mcrdl_redop_t op,
+                            mcrdl_algo_t algo, uint64_t seq, int dt, cudaStream_t s) {
+  const T* i = reinterpret_cast<const T*>(in);
+  T* o = reinterpret_cast<T*>(out);
+  switch (op) {
+    case MCRDL_SUM: return ar_typed<T, MCRDL_SUM>(c, i, o, n, algo, seq, dt, s);
+    case MCRDL_PROD: return ar_typed<T, MCRDL_PROD>(c, i, o, n, algo, seq, dt, s);
+    case MCRDL_MIN: return ar_typed<T, MCRDL_MIN>(c, i, o, n, algo, seq, dt, s);
+    case MCRDL_MAX: return ar_typed<T, MCRDL_MAX>(c, i, o, n, algo, seq, dt, s);
+  }
+  return set_error(MCRDL_ERR_VALIDATION, "unknown reduce op %d", int(op));
+}
+
+template <typename T, int OP>
+static mcrdl_status_t fused_typed(mcrdl_comm* c, const void* const* in_ptrs, void* const* out_ptrs,
+                                  const int64_t* counts, const int64_t* offs, int nmem,
+                                  int64_t total, uint64_t seq, int dt, cudaStream_t stream) {
+  constexpr int N = Pack<T>::N;
+  uint32_t epoch;
+  mcrdl_status_t st = begin_op(c, &epoch);
+  if (st != MCRDL_OK) return st;
+  const int64_t npk = (total + N - 1) / N;
+  const int64_t slot = (npk * 16 + 255) / 256 * 256;
+  if (slot * c->world > c->dc.half_bytes)
+    return set_error(MCRDL_ERR_VALIDATION, "fused all_reduce of %lld elements exceeds workspace",
+                     (long long)total);
+  const uint32_t sig = op_sig(kKindAllReduce, dt, OP, -2, uint64_t(total), seq);
+  const int G = grid_for(npk, c->num_sms, 64);
+  k_ar_fused<T, OP><<<G, kThreads, 0, stream>>>(
+      c->dc, reinterpret_cast<const T* const*>(in_ptrs), reinterpret_cast<T* const*>(out_ptrs), counts,
+      offs, nmem, total, slot, epoch, sig);
+  count_launch();
+  MCRDL_CUDA_CHECK(cudaGetLastError());
+  return MCRDL_OK;
+}
+
+template <typename T>
+static mcrdl_status_t fused_op(mcrdl_comm* c, const void* const* ip, void* const* op_, const int64_t* cn,
+                               const int64_t* of, int nm, int64_t total, mcrdl_redop_t op,
+                               uint64_t seq, int dt, cudaStream_t s) {
+  switch (op) {
+    case MCRDL_SUM: return fused_typed<T, MCRDL_SUM>(c, ip, op_, cn, of, nm, total, seq, dt, s);
+    case MCRDL_PROD: return fused_typed<T, MCRDL_PROD>(c, ip, op_, cn, of, nm, total, seq, dt, s);
+    case MCRDL_MIN: return fused_typed<T, MCRDL_MIN>(c, ip, op_, cn, of, nm, total, seq, dt, s);
+    case MCRDL_MAX: return fused_typed<T, MCRDL_MAX>(c, ip, op_, cn, of, nm, total, seq, dt, s);
+  }
+  return set_error(MCRDL_ERR_VALIDATION, "unknown reduce op %d", int(op));
+}
+
+}  // namespace mcrdl
+
+using namespace mcrdl;
+
+extern "C" {
+
+mcrdl_status_t mcrdl_all_reduce(mcrdl_comm* c, const void* in, void* out, uint64_t count,
+                                mcrdl_dtype_t dtype, mcrdl_redop_t op, mcrdl_algo_t algo,
+                                uint64_t seq, void* stream) {
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  if (count == 0) return mcrdl_barrier(c, seq, stream);
+  if (in == nullptr || out == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL buffer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t n = int64_t(count);
+  switch (dtype) {
+    case MCRDL_F32: return ar_op<float>(c, in, out, n, op, algo, seq, int(dtype), s);
+    case MCRDL_F64: return ar_op<double>(c, in, out, n, op, algo, seq, int(dtype), s);
+    case MCRDL_I32: return ar_op<int32_t>(c, in, out, n, op, algo, seq, int(dtype), s);
+    case MCRDL_I64: return ar_op<int64_t>(c, in, out, n, op, algo, seq, int(dtype), s);
+    case MCRDL_U8: return ar_op<uint8_t>(c, in, out, n, op, algo, seq, int(dtype), s);
+    case MCRDL_BF16: return ar_op<__nv_bfloat16>(c, in, out, n, op, algo, seq, int(dtype), s);
+  }
+  return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+}
+
+mcrdl_status_t mcrdl_all_reduce_fused(mcrdl_comm* c, const void* const* d_in_ptrs,
+                                      void* const* d_out_ptrs, const int64_t* d_counts,
+                                      const int64_t* d_offsets, int n, uint64_t total_count,
+                                      mcrdl_dtype_t dtype, mcrdl_redop_t op, mcrdl_algo_t algo,
+                                      uint64_t seq, void* stream) {
+  (void)algo;
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  if (n <= 0 || total_count == 0) return mcrdl_barrier(c, seq, stream);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t t = int64_t(total_count);
+  switch (dtype) {
+    case MCRDL_F32: return fused_op<float>(c, d_in_ptrs, d_out_ptrs, d_counts, d_offsets, n, t, op, seq, int(dtype), s);
+    case MCRDL_F64: return fused_op<double>(c, d_in_ptrs, d_out_ptrs, d_counts, d_offsets, n, t, op, seq, int(dtype), s);
+    case MCRDL_I32: return fused_op<int32_t>(c, d_in_ptrs, d_out_ptrs, d_counts, d_offsets, n, t, op, seq, int(dtype), s);
+    case MCRDL_I64: return fused_op<int64_t>(c, d_in_ptrs, d_out_ptrs, d_counts, d_offsets, n, t, op, seq, int(dtype), s);
+    case MCRDL_U8: return fused_op<uint8_t>(c, d_in_ptrs, d_out_ptrs, d_counts, d_offsets, n, t, op, seq, int(dtype), s);
+    case MCRDL_BF16:
+      return fused_op<__nv_bfloat16>(c, d_in_ptrs, d_out_ptrs, d_counts, d_offsets, n, t, op, seq, int(dtype), s);
+  }
+  return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+}
+
+}  // extern "C"

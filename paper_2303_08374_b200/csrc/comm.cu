@@ -1,0 +1,517 @@
+// Communicator lifecycle: symmetric VMM workspace, POSIX-fd handle exchange
+// over an abstract unix socket, peer mapping over NVLink, status/error plumbing.
+//
+// Reference counterpart: Runtime.init -> _build_transport (runtime.py:336-383)
+// and the TCP star bootstrap (transport.py:279-376). Here the host control
+// plane (the caller's allgather callback) carries only a job id and a barrier;
+// memory handles travel as file descriptors (SCM_RIGHTS) between the ranks'
+// processes, and every byte of payload afterwards moves GPU->GPU over NVLink.
+#include <cudaTypedefs.h>
+#include <errno.h>
+#include <poll.h>
+#include <stdio.h>
+#include <string.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <time.h>
+#include <unistd.h>
+
+#include <chrono>
+#include <map>
+#include <mutex>
+#include <random>
+#include <thread>
+
+#include "internal.h"
+
+namespace mcrdl {
+
+// ------------------------------------------------------------ error state
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+mcrdl_status_t set_error(mcrdl_status_t code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// ------------------------------------------------------------ driver API
+// Resolved through the runtime (cudaGetDriverEntryPoint) so this library has
+// no link-time dependency on libcuda and loads on hosts without a driver.
+struct Driver {
+  PFN_cuMemCreate memCreate = nullptr;
+  PFN_cuMemRelease memRelease = nullptr;
+  PFN_cuMemMap memMap = nullptr;
+  PFN_cuMemUnmap memUnmap = nullptr;
+  PFN_cuMemSetAccess memSetAccess = nullptr;
+  PFN_cuMemAddressReserve addrReserve = nullptr;
+  PFN_cuMemAddressFree addrFree = nullptr;
+  PFN_cuMemExportToShareableHandle exportHandle = nullptr;
+  PFN_cuMemImportFromShareableHandle importHandle = nullptr;
+  PFN_cuMemGetAllocationGranularity granularity = nullptr;
+  PFN_cuMulticastCreate mcCreate = nullptr;
+  PFN_cuMulticastAddDevice mcAddDevice = nullptr;
+  PFN_cuMulticastBindMem mcBindMem = nullptr;
+  PFN_cuMulticastUnbind mcUnbind = nullptr;
+  PFN_cuMulticastGetGranularity mcGranularity = nullptr;
+  PFN_cuGetErrorString errorString = nullptr;
+  bool loaded = false;
+};
+static Driver g_drv;
+static std::mutex g_drv_mu;
+
+template <typename F>
+static bool resolve(const char* name, F* out) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || fn == nullptr)
+    return false;
+  *out = reinterpret_cast<F>(fn);
+  return true;
+}
+
+static mcrdl_status_t load_driver() {
+  std::lock_guard<std::mutex> lk(g_drv_mu);
+  if (g_drv.loaded) return MCRDL_OK;
+  bool ok = resolve("cuMemCreate", &g_drv.memCreate) && resolve("cuMemRelease", &g_drv.memRelease) &&
+            resolve("cuMemMap", &g_drv.memMap) && resolve("cuMemUnmap", &g_drv.memUnmap) &&
+            resolve("cuMemSetAccess", &g_drv.memSetAccess) &&
+            resolve("cuMemAddressReserve", &g_drv.addrReserve) &&
+            resolve("cuMemAddressFree", &g_drv.addrFree) &&
+            resolve("cuMemExportToShareableHandle", &g_drv.exportHandle) &&
+            resolve("cuMemImportFromShareableHandle", &g_drv.importHandle) &&
+            resolve("cuMemGetAllocationGranularity", &g_drv.granularity) &&
+            resolve("cuGetErrorString", &g_drv.errorString);
+  if (!ok) return set_error(MCRDL_ERR_CUDA, "cannot resolve CUDA driver VMM entry points (no driver?)");
+  // Multicast is optional (NVLS).
+  resolve("cuMulticastCreate", &g_drv.mcCreate);
+  resolve("cuMulticastAddDevice", &g_drv.mcAddDevice);
+  resolve("cuMulticastBindMem", &g_drv.mcBindMem);
+  resolve("cuMulticastUnbind", &g_drv.mcUnbind);
+  resolve("cuMulticastGetGranularity", &g_drv.mcGranularity);
+  g_drv.loaded = true;
+  return MCRDL_OK;
+}
+
+static const char* cu_str(CUresult r) {
+  const char* s = nullptr;
+  if (g_drv.errorString) g_drv.errorString(r, &s);
+  return s ? s : "unknown CUDA driver error";
+}
+
+#define CU_CHECK(expr)                                                                  \
+  do {                                                                                  \
+    CUresult r_ = (expr);                                                               \
+    if (r_ != CUDA_SUCCESS)                                                             \
+      return set_error(MCRDL_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cu_str(r_),     \
+                       __FILE__, __LINE__);                                             \
+  } while (0)
+
+// ------------------------------------------------------------ bootstrap
+static mcrdl_status_t host_allgather(mcrdl_comm* c, const void* send, void* recv, size_t n) {
+  if (c->world == 1) {
+    memcpy(recv, send, n);
+    return MCRDL_OK;
+  }
+  if (c->allgather(c->ag_ctx, send, recv, n) != 0)
+    return set_error(MCRDL_ERR_BOOTSTRAP, "bootstrap allgather callback failed");
+  return MCRDL_OK;
+}
+
+static mcrdl_status_t host_barrier(mcrdl_comm* c) {
+  int x = c->rank, all[kMaxRanks];
+  return host_allgather(c, &x, all, sizeof(int));
+}
+
+// --------------------------------------------- fd passing (unix sockets)
+struct FdMsg {
+  uint32_t magic;
+  int32_t rank;
+  int32_t tag;
+  int32_t pad;
+};
+static constexpr uint32_t kFdMagic = 0x4D434644u;  // "MCFD"
+
+static socklen_t sock_name(sockaddr_un* a, uint64_t jobid, int rank) {
+  memset(a, 0, sizeof(*a));
+  a->sun_family = AF_UNIX;
+  // Abstract namespace: leading NUL, no filesystem entry.
+  int n = snprintf(a->sun_path + 1, sizeof(a->sun_path) - 1, "mcrdl-nvl-%016llx-%d",
+                   (unsigned long long)jobid, rank);
+  return socklen_t(offsetof(sockaddr_un, sun_path) + 1 + n);
+}
+
+// Messages that arrived early for a later exchange tag: (tag, rank) -> fd.
+static std::map<std::pair<int, int>, int> g_stash;
+static std::mutex g_stash_mu;
+static int g_fd_tag = 0;
+
+static mcrdl_status_t send_fd(uint64_t jobid, int to, int from, int tag, int fd, double timeout_s) {
+  sockaddr_un addr;
+  socklen_t len = sock_name(&addr, jobid, to);
+  auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    int s = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+    if (s < 0) return set_error(MCRDL_ERR_BOOTSTRAP, "socket(): %s", strerror(errno));
+    if (connect(s, reinterpret_cast<sockaddr*>(&addr), len) == 0) {
+      FdMsg m{kFdMagic, from, tag, 0};
+      iovec iov{&m, sizeof(m)};
+      char cbuf[CMSG_SPACE(sizeof(int))];
+      memset(cbuf, 0, sizeof(cbuf));
+      msghdr msg{};
+      msg.msg_iov = &iov;
+      msg.msg_iovlen = 1;
+      msg.msg_control = cbuf;
+      msg.msg_controllen = sizeof(cbuf);
+      cmsghdr* cm = CMSG_FIRSTHDR(&msg);
+      cm->cmsg_level = SOL_SOCKET;
+      cm->cmsg_type = SCM_RIGHTS;
+      cm->cmsg_len = CMSG_LEN(sizeof(int));
+      memcpy(CMSG_DATA(cm), &fd, sizeof(int));
+      ssize_t w = sendmsg(s, &msg, 0);
+      close(s);
+      if (w != ssize_t(sizeof(m)))
+        return set_error(MCRDL_ERR_PEER_DISCONNECTED, "sendmsg to rank %d: %s", to, strerror(errno));
+      return MCRDL_OK;
+    }
+    close(s);
+    double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > timeout_s)
+      return set_error(MCRDL_ERR_BOOTSTRAP, "connect to rank %d socket timed out: %s", to,
+                       strerror(errno));
+    std::this_thread::sleep_for(std::chrono::milliseconds(2));
+  }
+}
+
+static mcrdl_status_t recv_one_fd(int listen_fd, double timeout_s, FdMsg* m, int* fd) {
+  pollfd p{listen_fd, POLLIN, 0};
+  int pr = poll(&p, 1, int(timeout_s * 1000));
+  if (pr <= 0) return set_error(MCRDL_ERR_BOOTSTRAP, "timed out waiting for a peer fd");
+  int s = accept4(listen_fd, nullptr, nullptr, SOCK_CLOEXEC);
+  if (s < 0) return set_error(MCRDL_ERR_BOOTSTRAP, "accept(): %s", strerror(errno));
+  iovec iov{m, sizeof(*m)};
+  char cbuf[CMSG_SPACE(sizeof(int))];
+  msghdr msg{};
+  msg.msg_iov = &iov;
+  msg.msg_iovlen = 1;
+  msg.msg_control = cbuf;
+  msg.msg_controllen = sizeof(cbuf);
+  ssize_t r = recvmsg(s, &msg, MSG_WAITALL);
+  close(s);
+  cmsghdr* cm = CMSG_FIRSTHDR(&msg);
+  if (r != ssize_t(sizeof(*m)) || m->magic != kFdMagic || cm == nullptr ||
+      cm->cmsg_type != SCM_RIGHTS)
+    return set_error(MCRDL_ERR_PEER_DISCONNECTED, "malformed fd message from a peer");
+  memcpy(fd, CMSG_DATA(cm), sizeof(int));
+  return MCRDL_OK;
+}
+
+// Every rank sends `my_fd` to every peer and collects one fd per peer.
+static mcrdl_status_t exchange_fds(mcrdl_comm* c, int my_fd, int peer_fds[kMaxRanks]) {
+  const int tag = ++g_fd_tag;
+  const double tmo = double(c->timeout_ns) * 1e-9 + 30.0;
+  for (int r = 0; r < c->world; ++r) peer_fds[r] = -1;
+  peer_fds[c->rank] = my_fd;
+  for (int k = 1; k < c->world; ++k) {
+    int to = (c->rank + k) % c->world;
+    mcrdl_status_t st = send_fd(c->jobid, to, c->rank, tag, my_fd, tmo);
+    if (st != MCRDL_OK) return st;
+  }
+  int have = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_stash_mu);
+    for (int r = 0; r < c->world; ++r) {
+      auto it = g_stash.find({tag, r});
+      if (it != g_stash.end()) {
+        peer_fds[r] = it->second;
+        g_stash.erase(it);
+        ++have;
+      }
+    }
+  }
+  while (have < c->world - 1) {
+    FdMsg m;
+    int fd = -1;
+    mcrdl_status_t st = recv_one_fd(c->listen_fd, tmo, &m, &fd);
+    if (st != MCRDL_OK) return st;
+    if (m.tag == tag && m.rank >= 0 && m.rank < c->world && peer_fds[m.rank] < 0) {
+      peer_fds[m.rank] = fd;
+      ++have;
+    } else {
+      std::lock_guard<std::mutex> lk(g_stash_mu);
+      g_stash[{m.tag, m.rank}] = fd;
+    }
+  }
+  return MCRDL_OK;
+}
+
+// ------------------------------------------------------------ regions
+static CUmemAllocationProp alloc_prop(int dev) {
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = dev;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  return prop;
+}
+
+static mcrdl_status_t map_handle(mcrdl_comm* c, CUmemGenericAllocationHandle h, uint64_t bytes,
+                                 CUdeviceptr* out) {
+  CUdeviceptr va = 0;
+  CU_CHECK(g_drv.addrReserve(&va, bytes, c->gran, 0, 0));
+  CU_CHECK(g_drv.memMap(va, bytes, 0, h, 0));
+  CUmemAccessDesc d{};
+  d.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  d.location.id = c->device;
+  d.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  CU_CHECK(g_drv.memSetAccess(va, bytes, &d, 1));
+  *out = va;
+  return MCRDL_OK;
+}
+
+static void unmap_region(mcrdl_comm* c, Region& rg) {
+  for (int r = 0; r < c->world; ++r) {
+    if (rg.ptr[r]) {
+      g_drv.memUnmap(rg.ptr[r], rg.bytes);
+      g_drv.addrFree(rg.ptr[r], rg.bytes);
+      rg.ptr[r] = 0;
+    }
+    if (rg.handles[r]) {
+      g_drv.memRelease(rg.handles[r]);
+      rg.handles[r] = 0;
+    }
+  }
+  rg.local_handle = 0;
+}
+
+// Collective: allocate `bytes` on this GPU, export it, import every peer's
+// allocation and map all of them here.
+static mcrdl_status_t alloc_region(mcrdl_comm* c, uint64_t bytes, Region* rg) {
+  bytes = (bytes + c->gran - 1) / c->gran * c->gran;
+  rg->bytes = bytes;
+  CUmemAllocationProp prop = alloc_prop(c->device);
+  CUmemGenericAllocationHandle h = 0;
+  CU_CHECK(g_drv.memCreate(&h, bytes, &prop, 0));
+  rg->local_handle = h;
+  rg->handles[c->rank] = h;
+  int my_fd = -1;
+  CU_CHECK(g_drv.exportHandle(&my_fd, h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  int fds[kMaxRanks];
+  mcrdl_status_t st = exchange_fds(c, my_fd, fds);
+  if (st != MCRDL_OK) {
+    close(my_fd);
+    return st;
+  }
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    CUresult res = g_drv.importHandle(&rg->handles[r], reinterpret_cast<void*>(uintptr_t(fds[r])),
+                                      CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    close(fds[r]);
+    if (res != CUDA_SUCCESS)
+      return set_error(MCRDL_ERR_CUDA, "cuMemImportFromShareableHandle(rank %d): %s", r, cu_str(res));
+  }
+  close(my_fd);
+  for (int r = 0; r < c->world; ++r) {
+    st = map_handle(c, rg->handles[r], bytes, &rg->ptr[r]);
+    if (st != MCRDL_OK) return st;
+  }
+  return MCRDL_OK;
+}
+
+mcrdl_status_t begin_op(mcrdl_comm* comm, uint32_t* epoch) {
+  if (comm == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  if (comm->sticky != MCRDL_OK)
+    return set_error(comm->sticky, "communicator poisoned by an earlier device error (%s)",
+                     mcrdl_status_kind(comm->sticky));
+  if (comm->err_host && *reinterpret_cast<volatile int*>(comm->err_host) != 0) {
+    comm->sticky = *comm->err_host;
+    return set_error(comm->sticky, "communicator poisoned by an earlier device error (%s)",
+                     mcrdl_status_kind(comm->sticky));
+  }
+  comm->epoch += 1;
+  if (comm->epoch == 0) comm->epoch = 1;
+  *epoch = comm->epoch;
+  return MCRDL_OK;
+}
+
+}  // namespace mcrdl
+
+using namespace mcrdl;
+
+extern "C" {
+
+const char* mcrdl_last_error(void) { return g_last_error.c_str(); }
+
+int mcrdl_abi_version(void) { return MCRDL_NVL_ABI_VERSION; }
+
+uint64_t mcrdl_launch_count(void) { return g_launches.load(); }
+
+const char* mcrdl_status_kind(mcrdl_status_t s) {
+  switch (s) {
+    case MCRDL_OK: return "ok";
+    case MCRDL_ERR_VALIDATION: return "validation";
+    case MCRDL_ERR_ORDER_MISMATCH: return "order_mismatch";
+    case MCRDL_ERR_TIMEOUT: return "timeout";
+    case MCRDL_ERR_UNSUPPORTED: return "unsupported_operation";
+    case MCRDL_ERR_PEER_DISCONNECTED: return "peer_disconnected";
+    case MCRDL_ERR_CUDA: return "comm_error";
+    case MCRDL_ERR_BOOTSTRAP: return "bootstrap_timeout";
+    case MCRDL_ERR_LENGTH_MISMATCH: return "length_mismatch";
+    case MCRDL_ERR_NOT_INITIALIZED: return "not_initialized";
+    default: return "comm_error";
+  }
+}
+
+mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_device,
+                               mcrdl_allgather_fn allgather, void* ctx, uint64_t workspace_bytes,
+                               double timeout_secs) {
+  if (out == nullptr) return set_error(MCRDL_ERR_VALIDATION, "comm out-pointer is NULL");
+  *out = nullptr;
+  if (world < 1 || world > kMaxRanks)
+    return set_error(MCRDL_ERR_VALIDATION, "world size %d outside [1, %d]", world, kMaxRanks);
+  if (rank < 0 || rank >= world)
+    return set_error(MCRDL_ERR_VALIDATION, "rank %d outside world %d", rank, world);
+  if (world > 1 && allgather == nullptr)
+    return set_error(MCRDL_ERR_VALIDATION, "world > 1 needs a bootstrap allgather callback");
+  mcrdl_status_t st = load_driver();
+  if (st != MCRDL_OK) return st;
+  MCRDL_CUDA_CHECK(cudaSetDevice(cuda_device));
+  MCRDL_CUDA_CHECK(cudaFree(nullptr));  // make the primary context current
+
+  auto* c = new mcrdl_comm();
+  c->rank = rank;
+  c->world = world;
+  c->device = cuda_device;
+  c->allgather = allgather;
+  c->ag_ctx = ctx;
+  if (timeout_secs > 0) c->timeout_ns = uint64_t(timeout_secs * 1e9);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  auto fail = [&](mcrdl_status_t s) {
+    mcrdl_comm_destroy(c);
+    return s;
+  };
+
+  // Job id from rank 0 (fresh random per init) names the sockets.
+  std::random_device rd;
+  uint64_t mine = (uint64_t(rd()) << 32) ^ rd() ^ uint64_t(getpid());
+  uint64_t ids[kMaxRanks];
+  if ((st = host_allgather(c, &mine, ids, sizeof(uint64_t))) != MCRDL_OK) return fail(st);
+  c->jobid = ids[0];
+
+  if (world > 1) {
+    c->listen_fd = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+    sockaddr_un addr;
+    socklen_t len = sock_name(&addr, c->jobid, rank);
+    if (c->listen_fd < 0 || bind(c->listen_fd, reinterpret_cast<sockaddr*>(&addr), len) != 0 ||
+        listen(c->listen_fd, 128) != 0)
+      return fail(set_error(MCRDL_ERR_BOOTSTRAP, "unix socket setup failed: %s", strerror(errno)));
+  }
+  if ((st = host_barrier(c)) != MCRDL_OK) return fail(st);
+
+  CUmemAllocationProp prop = alloc_prop(cuda_device);
+  size_t g = 0;
+  CUresult r = g_drv.granularity(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
+  if (r != CUDA_SUCCESS)
+    return fail(set_error(MCRDL_ERR_CUDA, "cuMemGetAllocationGranularity: %s", cu_str(r)));
+  c->gran = g < (2u << 20) ? (2u << 20) : g;
+
+  if (workspace_bytes == 0) workspace_bytes = uint64_t(1) << 30;
+  workspace_bytes = (workspace_bytes + 2 * c->gran - 1) / (2 * c->gran) * (2 * c->gran);
+  c->ws_bytes = workspace_bytes;
+  if ((st = alloc_region(c, kPadBytes + workspace_bytes, &c->base)) != MCRDL_OK) return fail(st);
+  MCRDL_CUDA_CHECK(cudaMemset(reinterpret_cast<void*>(c->base.ptr[rank]), 0, kPadBytes));
+  MCRDL_CUDA_CHECK(cudaDeviceSynchronize());
+
+  MCRDL_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int),
+                                 cudaHostAllocMapped | cudaHostAllocPortable));
+  *c->err_host = 0;
+  MCRDL_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
+
+  c->dc.rank = rank;
+  c->dc.world = world;
+  c->dc.err = c->err_dev;
+  c->dc.timeout_ns = c->timeout_ns;
+  c->dc.half_bytes = int64_t(workspace_bytes / 2);
+  for (int q = 0; q < world; ++q) {
+    c->dc.pad[q] = reinterpret_cast<Pad*>(c->base.ptr[q]);
+    c->dc.ws[q] = reinterpret_cast<uint8_t*>(c->base.ptr[q]) + kPadBytes;
+  }
+  // Nobody may signal into a pad before its owner zeroed it.
+  if ((st = host_barrier(c)) != MCRDL_OK) return fail(st);
+  *out = c;
+  return MCRDL_OK;
+}
+
+mcrdl_status_t mcrdl_comm_destroy(mcrdl_comm* c) {
+  if (c == nullptr) return MCRDL_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto& rg : c->symm) unmap_region(c, rg);
+  c->symm.clear();
+  unmap_region(c, c->base);
+  if (c->err_host) cudaFreeHost(c->err_host);
+  if (c->listen_fd >= 0) close(c->listen_fd);
+  delete c;
+  return MCRDL_OK;
+}
+
+mcrdl_status_t mcrdl_comm_caps(const mcrdl_comm* c, mcrdl_caps_t* caps) {
+  if (c == nullptr || caps == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL argument");
+  memset(caps, 0, sizeof(*caps));
+  caps->rank = c->rank;
+  caps->world = c->world;
+  caps->device = c->device;
+  caps->num_sms = c->num_sms;
+  caps->nvls_supported = c->nvls.ok ? 1 : 0;
+  caps->workspace_bytes = c->ws_bytes;
+  caps->max_oneshot_bytes = uint64_t(c->dc.half_bytes) / uint64_t(c->world) / 256 * 256;
+  caps->max_twoshot_chunk = uint64_t(c->dc.half_bytes) / 2 / 256 * 256;
+  return MCRDL_OK;
+}
+
+mcrdl_status_t mcrdl_comm_status(mcrdl_comm* c) {
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  int e = *reinterpret_cast<volatile int*>(c->err_host);
+  if (e != 0 && c->sticky == MCRDL_OK) c->sticky = e;
+  if (c->sticky != MCRDL_OK)
+    return set_error(c->sticky, "device reported %s", mcrdl_status_kind(c->sticky));
+  return MCRDL_OK;
+}
+
+mcrdl_status_t mcrdl_symm_alloc(mcrdl_comm* c, uint64_t bytes, void** local_ptr) {
+  if (c == nullptr || local_ptr == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL argument");
+  if (bytes == 0) bytes = 1;
+  Region rg;
+  mcrdl_status_t st = alloc_region(c, bytes, &rg);
+  if (st != MCRDL_OK) {
+    unmap_region(c, rg);
+    return st;
+  }
+  MCRDL_CUDA_CHECK(cudaMemset(reinterpret_cast<void*>(rg.ptr[c->rank]), 0, rg.bytes));
+  c->symm.push_back(rg);
+  *local_ptr = reinterpret_cast<void*>(rg.ptr[c->rank]);
+  return MCRDL_OK;
+}
+
+mcrdl_status_t mcrdl_symm_free(mcrdl_comm* c, void* local_ptr) {
+  if (c == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL communicator");
+  for (size_t i = 0; i < c->symm.size(); ++i) {
+    if (reinterpret_cast<void*>(c->symm[i].ptr[c->rank]) == local_ptr) {
+      cudaDeviceSynchronize();
+      unmap_region(c, c->symm[i]);
+      c->symm.erase(c->symm.begin() + i);
+      return MCRDL_OK;
+    }
+  }
+  return set_error(MCRDL_ERR_VALIDATION, "pointer is not a symmetric allocation of this comm");
+}
+
+}  // extern "C"

@@ -1,0 +1,323 @@
+// Device-side building blocks shared by every collective kernel.
+//
+// Memory model of the backend:
+//  * Every rank owns one cuMem VMM region = [signal pad | workspace]. Every
+//    peer's region is mapped into every rank's address space, so a kernel
+//    reaches a peer with plain ld/st over NVLink (NVSwitch routes them).
+//  * The workspace is split into two halves; op with epoch e uses half e&1.
+//    Every op ends only after receiving a flag from every peer, so when a rank
+//    starts op e+2 in half (e&1), every peer has finished op e (stream order).
+//  * Flags are 64-bit words in the RECEIVER's pad, one per (parity, block,
+//    sender), value = epoch<<32 | sig20<<12 | step12. `sig` folds the op
+//    signature (kind, dtype, op, root, count, reference seq) — the device
+//    restatement of the reference's header agreement (collectives.py:178-285):
+//    a rank that posted a different op at the same slot sees a sig mismatch
+//    and raises ORDER_MISMATCH instead of corrupting data.
+//  * Release/acquire at .sys scope; every spin is bounded by the comm timeout
+//    (reference: MCRDL_TIMEOUT_SECS, runtime.py:65) and by a peer abort word.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mcrdl_nvl.h"
+
+namespace mcrdl {
+
+constexpr int kMaxRanks = MCRDL_MAX_RANKS;
+constexpr int kMaxBlocks = 512;  // flag slots per parity
+constexpr int kThreads = 512;
+
+struct Pad {
+  uint64_t flag[2][kMaxBlocks][kMaxRanks];   // data-ready, phase 1
+  uint64_t flag2[2][kMaxBlocks][kMaxRanks];  // data-ready, phase 2
+  uint64_t ack[2][kMaxBlocks][kMaxRanks];    // slot consumed (multi-round)
+  uint64_t abort_word[2][2];                 // [par] = {epoch, code}
+};
+constexpr size_t kPadBytes = size_t(1) << 20;  // workspace starts 1 MiB into the region
+static_assert(sizeof(Pad) <= kPadBytes, "pad too large");
+
+struct DevComm {
+  uint8_t* ws[kMaxRanks];  // rank r's workspace, mapped in this address space
+  Pad* pad[kMaxRanks];     // rank r's signal pad
+  int* err;                // host-mapped latched error word
+  uint64_t timeout_ns;
+  int64_t half_bytes;      // bytes per workspace half
+  int rank;
+  int world;
+};
+
+// ------------------------------------------------------------ primitives
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// 16-byte loads/stores. Workspace reads use .cg (L2, the coherence point for
+// peer writes); user-buffer reads use the default path.
+__device__ __forceinline__ uint4 ld16(const void* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ uint4 ld16_cg(const void* p) {
+  return __ldcg(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ void st16(void* p, const uint4& v) { *reinterpret_cast<uint4*>(p) = v; }
+
+__device__ __forceinline__ uint64_t make_flag(uint32_t epoch, uint32_t sig, uint32_t step) {
+  return (uint64_t(epoch) << 32) | (uint64_t(sig & 0xFFFFFu) << 12) | uint64_t(step & 0xFFFu);
+}
+
+__host__ __device__ __forceinline__ uint32_t mix32(uint32_t h, uint64_t v) {
+  // FNV-1a style mix of a 64-bit value into a 32-bit hash.
+  for (int i = 0; i < 8; ++i) {
+    h ^= uint32_t((v >> (8 * i)) & 0xFF);
+    h *= 16777619u;
+  }
+  return h;
+}
+
+// Per-CTA shared copy of the peer pointer tables. Indexing the kernel-param
+// arrays with a runtime rank would spill DevComm to local memory; the staged
+// copy is loaded with constant indices once per CTA.
+struct SComm {
+  uint8_t* ws[kMaxRanks];
+  Pad* pad[kMaxRanks];
+};
+__device__ __forceinline__ void stage_comm(const DevComm& c, SComm& s) {
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int r = 0; r < kMaxRanks; ++r) {
+      s.ws[r] = c.ws[r];
+      s.pad[r] = c.pad[r];
+    }
+  }
+}
+
+// Record an error: latch it in the host-visible word and tell every peer to
+// stop spinning on this op (abort word carries the epoch + code).
+static __device__ __noinline__ void raise_error(Pad* const* pads, int world, int* err, int code,
+                                                uint32_t epoch) {
+  const int par = epoch & 1;
+  atomicCAS(err, 0, code);
+  for (int r = 0; r < world; ++r) {
+    st_relaxed_sys(&pads[r]->abort_word[par][1], uint64_t(code));
+    __threadfence_system();
+    st_release_sys(&pads[r]->abort_word[par][0], uint64_t(epoch));
+  }
+}
+
+// Spin until the flag at `p` carries (epoch, sig, >= step). Returns MCRDL_OK
+// or an error code; never spins past the timeout or a peer abort (`me` is
+// the local pad).
+static __device__ __noinline__ int wait_flag(const uint64_t* p, const Pad* me, uint64_t timeout_ns,
+                                             uint32_t epoch, uint32_t sig, uint32_t step) {
+  const int par = epoch & 1;
+  uint64_t start = 0;
+  int spins = 0;
+  for (;;) {
+    const uint64_t v = ld_acquire_sys(p);
+    if (uint32_t(v >> 32) == epoch) {
+      const uint32_t lo = uint32_t(v);
+      if ((lo >> 12) != (sig & 0xFFFFFu)) return MCRDL_ERR_ORDER_MISMATCH;
+      if ((lo & 0xFFFu) >= (step & 0xFFFu)) return MCRDL_OK;
+    }
+    if (++spins >= 32) {
+      spins = 0;
+      if (ld_acquire_sys(&me->abort_word[par][0]) == epoch) {
+        int code = int(ld_relaxed_sys(&me->abort_word[par][1]));
+        return code ? code : MCRDL_ERR_INTERNAL;
+      }
+      const uint64_t now = globaltimer_ns();
+      if (start == 0) {
+        start = now;
+      } else if (now - start > timeout_ns) {
+        return MCRDL_ERR_TIMEOUT;
+      }
+    }
+  }
+}
+
+// Threads [0, world) except `rank` publish flag value `val` into peer r's
+// array slot [par][slot][rank]. Caller must __syncthreads() before (so every
+// thread's payload stores precede the release).
+__device__ __forceinline__ void publish(uint64_t* peer_slot, uint64_t val) {
+  __threadfence_system();
+  st_release_sys(peer_slot, val);
+}
+
+// ------------------------------------------------------------ reduce ops
+template <typename T>
+struct AccT {
+  using type = T;
+};
+template <>
+struct AccT<__nv_bfloat16> {
+  using type = float;
+};
+
+template <typename A>
+__device__ __forceinline__ A op_sum(A a, A b) { return a + b; }
+template <>
+__device__ __forceinline__ int32_t op_sum(int32_t a, int32_t b) {
+  return int32_t(uint32_t(a) + uint32_t(b));
+}
+template <>
+__device__ __forceinline__ int64_t op_sum(int64_t a, int64_t b) {
+  return int64_t(uint64_t(a) + uint64_t(b));
+}
+template <>
+__device__ __forceinline__ uint8_t op_sum(uint8_t a, uint8_t b) { return uint8_t(a + b); }
+
+template <typename A>
+__device__ __forceinline__ A op_prod(A a, A b) { return a * b; }
+template <>
+__device__ __forceinline__ int32_t op_prod(int32_t a, int32_t b) {
+  return int32_t(uint32_t(a) * uint32_t(b));
+}
+template <>
+__device__ __forceinline__ int64_t op_prod(int64_t a, int64_t b) {
+  return int64_t(uint64_t(a) * uint64_t(b));
+}
+template <>
+__device__ __forceinline__ uint8_t op_prod(uint8_t a, uint8_t b) { return uint8_t(a * b); }
+
+// numpy minimum/maximum semantics: NaN propagates, ties return the second
+// operand (np.minimum(0.0, -0.0) == -0.0).
+template <typename A>
+__device__ __forceinline__ A op_min(A a, A b) { return (a != a || a < b) ? a : b; }
+template <typename A>
+__device__ __forceinline__ A op_max(A a, A b) { return (a != a || a > b) ? a : b; }
+
+template <int OP, typename A>
+__device__ __forceinline__ A apply_op(A a, A b) {
+  if constexpr (OP == MCRDL_SUM) return op_sum<A>(a, b);
+  else if constexpr (OP == MCRDL_PROD) return op_prod<A>(a, b);
+  else if constexpr (OP == MCRDL_MIN) return op_min<A>(a, b);
+  else return op_max<A>(a, b);
+}
+
+// A 16-byte pack of T, unpacked into accumulator registers.
+template <typename T>
+struct Pack {
+  static constexpr int N = 16 / int(sizeof(T));
+  using A = typename AccT<T>::type;
+  A v[N];
+
+  __device__ __forceinline__ void from_raw(const uint4& raw) {
+    const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = to_acc(e[i]);
+  }
+  __device__ __forceinline__ uint4 to_raw() const {
+    uint4 raw;
+    T* e = reinterpret_cast<T*>(&raw);
+#pragma unroll
+    for (int i = 0; i < N; ++i) e[i] = from_acc(v[i]);
+    return raw;
+  }
+  template <int OP>
+  __device__ __forceinline__ void fold(const uint4& raw) {
+    const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = apply_op<OP, A>(v[i], to_acc(e[i]));
+  }
+  static __device__ __forceinline__ A to_acc(T x) {
+    if constexpr (sizeof(T) == 2) return __bfloat162float(x);
+    else return x;
+  }
+  static __device__ __forceinline__ T from_acc(A x) {
+    if constexpr (sizeof(T) == 2) return __float2bfloat16_rn(x);  // one RNE rounding
+    else return x;
+  }
+};
+
+// Load pack i of an n-element array; partial/misaligned packs go element-wise
+// (unused lanes zero). VEC: the base pointer is 16-byte aligned.
+template <typename T, bool VEC>
+__device__ __forceinline__ uint4 load_pack(const T* base, int64_t i, int64_t n) {
+  constexpr int N = 16 / int(sizeof(T));
+  if (VEC && (i + 1) * N <= n) return ld16(base + i * N);
+  uint4 raw = make_uint4(0, 0, 0, 0);
+  T* e = reinterpret_cast<T*>(&raw);
+  const int64_t lim = n - i * N;
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+    if (k < lim) e[k] = base[i * N + k];
+  return raw;
+}
+template <typename T, bool VEC>
+__device__ __forceinline__ void store_pack(T* base, int64_t i, int64_t n, const uint4& raw) {
+  constexpr int N = 16 / int(sizeof(T));
+  if (VEC && (i + 1) * N <= n) {
+    st16(base + i * N, raw);
+    return;
+  }
+  const T* e = reinterpret_cast<const T*>(&raw);
+  const int64_t lim = n - i * N;
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+    if (k < lim) base[i * N + k] = e[k];
+}
+
+// Block-cooperative byte copy, widest access the alignment of dst, src and n
+// allows. Loads are batched (UNROLL in flight per thread) before the stores.
+template <int UNROLL = 4>
+__device__ __forceinline__ void block_copy(uint8_t* dst, const uint8_t* src, int64_t n) {
+  if (n <= 0 || dst == src) return;
+  const uintptr_t a = uintptr_t(dst) | uintptr_t(src);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  int64_t done = 0;
+  if ((a & 15) == 0) {
+    const int64_t np = n >> 4;
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    int64_t i = tid;
+    for (; i + (UNROLL - 1) * nt < np; i += UNROLL * nt) {
+      uint4 v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) v[u] = __ldcg(s + i + u * nt);
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) d[i + u * nt] = v[u];
+    }
+    for (; i < np; i += nt) d[i] = __ldcg(s + i);
+    done = np << 4;
+  } else if ((a & 7) == 0) {
+    const int64_t np = n >> 3;
+    const uint2* s = reinterpret_cast<const uint2*>(src);
+    uint2* d = reinterpret_cast<uint2*>(dst);
+    for (int64_t i = tid; i < np; i += nt) d[i] = __ldcg(s + i);
+    done = np << 3;
+  } else if ((a & 3) == 0) {
+    const int64_t np = n >> 2;
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+    for (int64_t i = tid; i < np; i += nt) d[i] = __ldcg(s + i);
+    done = np << 2;
+  }
+  for (int64_t i = done + tid; i < n; i += nt) dst[i] = src[i];
+}
+
+// [s, e) share of `len` bytes for block b of G (16-byte aligned starts).
+__device__ __forceinline__ void byte_share(int64_t len, int b, int G, int64_t& s, int64_t& e) {
+  int64_t chunk = (len + G - 1) / G;
+  chunk = (chunk + 15) & ~int64_t(15);
+  s = min(len, int64_t(b) * chunk);
+  e = min(len, s + chunk);
+}
+
+}  // namespace mcrdl

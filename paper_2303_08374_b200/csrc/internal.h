@@ -1,0 +1,126 @@
+// Host-side communicator state and helpers shared by the launch files.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/mcrdl_nvl.h"
+#include "common.cuh"
+
+namespace mcrdl {
+
+// One peer-mapped VMM region (the base pad+workspace or a user symmetric alloc).
+struct Region {
+  uint64_t bytes = 0;  // mapped size (granularity-rounded)
+  CUmemGenericAllocationHandle local_handle = 0;
+  CUmemGenericAllocationHandle handles[kMaxRanks] = {};
+  CUdeviceptr ptr[kMaxRanks] = {};  // rank r's region mapped here
+};
+
+struct Nvls {
+  bool ok = false;
+  CUmemGenericAllocationHandle mc_handle = 0;
+  CUdeviceptr mc_ptr = 0;  // multicast VA covering the workspace
+  uint64_t bytes = 0;
+};
+
+}  // namespace mcrdl
+
+struct mcrdl_comm {
+  int rank = 0;
+  int world = 1;
+  int device = 0;
+  int num_sms = 0;
+  mcrdl_allgather_fn allgather = nullptr;
+  void* ag_ctx = nullptr;
+  uint64_t jobid = 0;
+  int listen_fd = -1;
+  uint64_t gran = 0;
+  mcrdl::Region base;                 // [pad | workspace]
+  std::vector<mcrdl::Region> symm;    // user symmetric allocations
+  mcrdl::Nvls nvls;
+  int* err_host = nullptr;            // cudaHostAllocMapped
+  int* err_dev = nullptr;
+  uint32_t epoch = 0;                 // launches so far (flag epoch)
+  uint64_t timeout_ns = 30ull * 1000000000ull;
+  uint64_t ws_bytes = 0;
+  mcrdl::DevComm dc{};
+  int sticky = MCRDL_OK;              // poisoned after a device error
+};
+
+namespace mcrdl {
+
+// Thread-local last-error message + return code.
+mcrdl_status_t set_error(mcrdl_status_t code, const char* fmt, ...);
+void count_launch();
+
+#define MCRDL_CUDA_CHECK(expr)                                                        \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return ::mcrdl::set_error(MCRDL_ERR_CUDA, "%s failed: %s (%s:%d)", #expr,      \
+                                cudaGetErrorString(e_), __FILE__, __LINE__);          \
+  } while (0)
+
+// Validates the comm and returns its next epoch (>= 1).
+mcrdl_status_t begin_op(mcrdl_comm* comm, uint32_t* epoch);
+
+inline int elem_size(mcrdl_dtype_t dt) {
+  switch (dt) {
+    case MCRDL_F32: return 4;
+    case MCRDL_F64: return 8;
+    case MCRDL_I32: return 4;
+    case MCRDL_I64: return 8;
+    case MCRDL_U8: return 1;
+    case MCRDL_BF16: return 2;
+  }
+  return 0;
+}
+
+inline uint32_t op_sig(int kind, int dtype, int op, int root, uint64_t count, uint64_t seq) {
+  uint32_t h = 2166136261u;
+  h = mix32(h, uint64_t(kind));
+  h = mix32(h, uint64_t(dtype));
+  h = mix32(h, uint64_t(op));
+  h = mix32(h, uint64_t(int64_t(root)));
+  h = mix32(h, count);
+  h = mix32(h, seq);
+  return h;
+}
+
+// Kind tags folded into signatures (CommOpKind order, core.py:89-104).
+enum KindTag : int {
+  kKindBcast = 2,
+  kKindAllReduce = 4,
+  kKindGatherv = 6,
+  kKindAllGatherv = 10,
+  kKindA2ASingle = 12,
+  kKindA2AList = 13,
+  kKindA2AV = 14,
+  kKindBarrier = 99,
+};
+
+// Exchange engine entry (exchange.cu): per-peer send/recv byte spans.
+struct ExchangeSpec {
+  const uint8_t* sptr[kMaxRanks];
+  int64_t sbytes[kMaxRanks];
+  uint8_t* rptr[kMaxRanks];
+  int64_t rbytes[kMaxRanks];
+  const int64_t* d_counts;  // optional device counts (elements)
+  const uint8_t* in_base;
+  uint8_t* out_base;
+  int64_t in_count;  // element capacities for device-count bounds checks
+  int64_t out_count;
+  int esize;
+  uint32_t sig_base;
+};
+mcrdl_status_t launch_exchange(mcrdl_comm* comm, const ExchangeSpec& spec, int64_t total_hint,
+                               cudaStream_t stream);
+
+}  // namespace mcrdl

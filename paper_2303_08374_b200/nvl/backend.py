@@ -1,0 +1,509 @@
+"""The NVLink/NVSwitch backend: one communicator per backend id, one lane
+CUDA stream, and a C-ABI call per collective.
+
+Reference seam: ``BackendConfig.transport`` ->
+``Runtime._build_transport`` (runtime.py:359-383) and
+``BackendInstance.post/_process/execute`` (runtime.py:142-277). The
+reference's lane THREAD becomes a lane STREAM ("records a CUDA
+event e onto the communication stream"); its inline fast path (runtime.py:
+150-168) is the default here because a post only enqueues device work.
+
+Buffers that are CUDA tensors run zero-copy. Host buffers (numpy, as in the
+reference) are staged through pinned memory on the lane stream and copied
+back when the handle settles. There is no host/CPU execution path: if the
+native library or a CUDA device is missing, init raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import time
+from ctypes import byref, c_void_p
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from ..collectives import ALGO_CODES, AlgorithmPolicy, canonical
+from ..core import (Buffer, CommOpKind, CommRequest, CompletionEvent, DType, HandleState,
+                    WorkHandle)
+from ..errors import (BackendFinalized, CommError, NativeBackendMissing, PendingAfterTimeout,
+                      UnsupportedOperation, ValidationError)
+from . import _lib
+from .bootstrap import StoreBootstrap, make_store
+
+try:
+    import torch
+except Exception:  # pragma: no cover
+    torch = None  # type: ignore[assignment]
+
+
+class NvlComm:
+    """Owner of one native communicator (symmetric workspace + signal pads)."""
+
+    def __init__(self, rank: int, world: int, device: int, bootstrap: Optional[StoreBootstrap],
+                 workspace_bytes: int, timeout: float):
+        self.lib = _lib.load()
+        self.rank, self.world, self.device = rank, world, device
+        self._bootstrap = bootstrap  # keeps the ctypes callback alive
+        handle = c_void_p()
+        cb = bootstrap.c_callback if bootstrap is not None else ctypes.cast(None, _lib.ALLGATHER_FN)
+        _lib.check(self.lib.mcrdl_comm_init(byref(handle), rank, world, device, cb, None,
+                                            int(workspace_bytes), float(timeout)))
+        self.handle = handle
+        caps = _lib.Caps()
+        _lib.check(self.lib.mcrdl_comm_caps(handle, byref(caps)))
+        self.caps = caps
+
+    def status(self) -> None:
+        _lib.check(self.lib.mcrdl_comm_status(self.handle))
+
+    def destroy(self) -> None:
+        if self.handle:
+            self.lib.mcrdl_comm_destroy(self.handle)
+            self.handle = c_void_p()
+
+
+class _Staging:
+    """Maps request Buffers to device tensors for one op; host buffers go
+    through pinned memory on the lane stream and are copied back at settle."""
+
+    def __init__(self, device, stream):
+        self.device = device
+        self.stream = stream
+        self.keep: list = []
+        self.copy_back: list = []  # (Buffer, pinned host tensor)
+        self._cache = {}
+
+    def dev(self, buf: Optional[Buffer], *, upload: bool = True, download: bool = False):
+        if buf is None:
+            return None
+        key = id(buf)
+        if key in self._cache:
+            t = self._cache[key]
+            if download and not any(b is buf for b, _ in self.copy_back):
+                self._download(buf, t)
+            return t
+        if buf.is_device:
+            t = buf.array
+            if t.device.index != self.device:
+                raise ValidationError("buffer", f"tensor on cuda:{t.device.index}, backend uses "
+                                      f"cuda:{self.device}")
+            t.record_stream(self.stream)
+        else:
+            host = buf.array if buf.is_tensor else torch.from_numpy(buf.array)
+            t = torch.empty(host.shape[0], dtype=host.dtype, device=self.device)
+            if upload and host.shape[0]:
+                pinned = host.pin_memory() if not host.is_pinned() else host
+                t.copy_(pinned, non_blocking=True)
+                self.keep.append(pinned)
+            if download:
+                self._download(buf, t)
+        self._cache[key] = t
+        return t
+
+    def _download(self, buf: Buffer, t) -> None:
+        if buf.is_device:
+            return
+        pinned = torch.empty(t.shape[0], dtype=t.dtype, pin_memory=True)
+        self.copy_back.append((buf, pinned, t))
+
+    def issue_downloads(self) -> None:
+        for _buf, pinned, t in self.copy_back:
+            if t.shape[0]:
+                pinned.copy_(t, non_blocking=True)
+
+    def scratch(self, count: int, dtype: DType):
+        return torch.empty(max(count, 0), dtype=dtype.torch_dtype, device=self.device)
+
+    def finish(self) -> None:
+        for buf, pinned, _t in self.copy_back:
+            if buf.is_tensor:
+                buf.array.copy_(pinned)
+            else:
+                np.copyto(buf.array, pinned.numpy())
+        self.copy_back.clear()
+        self.keep.clear()
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else (int(t.data_ptr()) or None)
+
+
+class NvlBackendInstance:
+    """A registered ``transport="nvlink"`` backend."""
+
+    transport_name = "nvlink"
+
+    def __init__(self, config, runtime):
+        if torch is None or not torch.cuda.is_available():
+            raise NativeBackendMissing(
+                "the nvlink transport needs a CUDA device (B200); no CPU fallback exists")
+        _lib.load()
+        if getattr(config, "compression", None) is not None:
+            raise UnsupportedOperation("compression middleware is not implemented on nvlink")
+        self.config = config
+        self.name = config.name
+        self.runtime = runtime
+        self.policy: AlgorithmPolicy = config.policy or AlgorithmPolicy()
+        self.state = "initialized"
+        self.collectives_executed = 0
+        self._seq = 0
+        self._lock = threading.RLock()  # one host thread at a time per communicator
+        self._pending: List[WorkHandle] = []
+        self._errors: List[BaseException] = []
+        n_dev = torch.cuda.device_count()
+        dev = config.device if config.device is not None else runtime.local_device
+        if dev is None:
+            dev = runtime.rank % max(n_dev, 1)
+        self.device = int(dev)
+        torch.cuda.set_device(self.device)
+        self.stream = torch.cuda.Stream(device=self.device)
+        boot = None
+        if runtime.world_size > 1:
+            store = runtime._control_store(config)
+            boot = StoreBootstrap(runtime.rank, runtime.world_size, store,
+                                  prefix=f"mcrdl-nvl/{self.name}/{runtime._init_generation}")
+        ws = config.workspace_bytes or runtime.default_workspace_bytes
+        self.comm = NvlComm(runtime.rank, runtime.world_size, self.device, boot, ws,
+                            runtime.timeout)
+
+    # ------------------------------------------------------------ properties
+    @property
+    def rank(self) -> int:
+        return self.runtime.rank
+
+    @property
+    def world_size(self) -> int:
+        return self.runtime.world_size
+
+    def next_seq(self) -> int:
+        with self._lock:
+            s = self._seq
+            self._seq += 1
+            return s
+
+    def pending_count(self) -> int:
+        with self._lock:
+            self._reap()
+            return sum(1 for h in self._pending if not h.test())
+
+    def drain_errors(self) -> List[BaseException]:
+        with self._lock:
+            errs, self._errors = self._errors, []
+            return errs
+
+    # ---------------------------------------------------------------- posting
+    def _algo_code(self, kind: CommOpKind, nbytes: int) -> int:
+        name = self.policy.algorithm(kind)
+        if name == "auto" and self.runtime.tuning_table is not None:
+            t = self.runtime.tuning_table.algorithm_for(kind, self.world_size, nbytes, self.name)
+            if t is not None:
+                name = canonical(kind, t)
+        return ALGO_CODES.get(name, 0)
+
+    def post(self, request: CommRequest) -> WorkHandle:
+        if self.state != "initialized":
+            raise BackendFinalized(f"backend {self.name!r} is {self.state}")
+        handle = WorkHandle(self.name, request)
+        with self._lock:
+            request.seq = self._seq
+            self._seq += 1
+            handle.mark_in_progress()
+            self._reap()
+            caller = torch.cuda.current_stream(self.device)
+            lane = self.stream
+            lane.wait_stream(caller)
+            st = _Staging(self.device, lane)
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(lane):
+                t0.record(lane)
+                try:
+                    self._launch(request, st, int(lane.cuda_stream))
+                except BaseException as exc:
+                    self._fail_now(handle, request, exc)
+                    raise
+                st.issue_downloads()
+                t1.record(lane)
+            self._arm(handle, request, st, t0, t1)
+        return handle
+
+    def post_fused(self, members: Sequence[CommRequest], ready_events: Sequence,
+                   flush_request: CommRequest) -> WorkHandle:
+        """One launch: pack -> all_reduce -> unpack for fusion members
+        (middleware FusionManager flush, middleware.py:311-344)."""
+        handle = WorkHandle(self.name, flush_request)
+        with self._lock:
+            flush_request.seq = self._seq
+            self._seq += 1
+            handle.mark_in_progress()
+            lane = self.stream
+            for ev in ready_events:
+                if ev is not None:
+                    lane.wait_event(ev)
+            st = _Staging(self.device, lane)
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.device(self.device), torch.cuda.stream(lane):
+                t0.record(lane)
+                dtype = members[0].input.dtype
+                esz = dtype.size_bytes
+                align = max(1, 16 // esz)
+                ins, outs, counts, offs = [], [], [], []
+                off = 0
+                for m in members:
+                    i = st.dev(m.input)
+                    o = st.dev(m.output, upload=m.output is m.input, download=True)
+                    ins.append(_ptr(i) or 0)
+                    outs.append(_ptr(o) or 0)
+                    counts.append(m.input.count)
+                    offs.append(off)
+                    off += (m.input.count + align - 1) // align * align
+                table = torch.tensor([ins, outs, counts, offs], dtype=torch.int64).pin_memory()
+                dtable = table.to(self.device, non_blocking=True)
+                st.keep.extend([table, dtable])
+                n = len(members)
+                base = int(dtable.data_ptr())
+                try:
+                    _lib.check(self.comm.lib.mcrdl_all_reduce_fused(
+                        self.comm.handle, base, base + 8 * n, base + 16 * n, base + 24 * n, n,
+                        off, dtype.code, flush_request.op.code,
+                        self._algo_code(CommOpKind.all_reduce, off * esz), flush_request.seq,
+                        int(lane.cuda_stream)))
+                except BaseException as exc:
+                    self._fail_now(handle, flush_request, exc)
+                    raise
+                st.issue_downloads()
+                t1.record(lane)
+            self._arm(handle, flush_request, st, t0, t1)
+        return handle
+
+    def _fail_now(self, handle: WorkHandle, request: CommRequest, exc: BaseException) -> None:
+        self._errors.append(exc)
+        for b in request.unique_buffers():
+            b._checkin()
+        handle.fail(exc)
+
+    def _arm(self, handle: WorkHandle, request: CommRequest, st: _Staging, t0, t1) -> None:
+        handle.event = t1
+        log = self.runtime.comm_log
+
+        def finalizer() -> None:
+            try:
+                st.finish()
+                self.comm.status()
+            except BaseException as exc:
+                with self._lock:
+                    self._errors.append(exc)
+                raise
+            finally:
+                for b in request.unique_buffers():
+                    b._checkin()
+            self.collectives_executed += 1
+            members = getattr(request, "_fused_members", 0)
+            from ..dispatch import message_bytes
+            from ..middleware import LogRecord
+
+            log.emit(LogRecord(ts_us=log.now_us(), rank=self.rank, op=request.kind.value,
+                               backend=self.name,
+                               bytes=message_bytes(request, self.world_size),
+                               dur_us=max(t0.elapsed_time(t1) * 1e3, 0.001),
+                               seq=request.seq or 0, fused=members > 0,
+                               members=members or 1,
+                               algorithm=getattr(request, "_algorithm", None)))
+
+        handle._finalizer = finalizer
+        self._pending.append(handle)
+
+    def _reap(self) -> None:
+        keep = []
+        for h in self._pending:
+            if not h.test():
+                keep.append(h)
+        self._pending = keep
+
+    def record_event(self) -> CompletionEvent:
+        with self._lock:
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+            pending = list(self._pending)
+        ce = CompletionEvent(self.name, cuda_event=ev)
+        ce._pending = pending  # type: ignore[attr-defined]
+        return ce
+
+    def settle(self, event: CompletionEvent) -> None:
+        """After `event` fired: settle every handle it covers."""
+        for h in getattr(event, "_pending", []):
+            h.test() if h.event is not None else None
+            if not h.test():
+                h._settle()
+        with self._lock:
+            self._reap()
+
+    def finalize(self, timeout: float) -> None:
+        if self.state == "finalized":
+            return
+        ev = self.record_event()
+        if not ev.wait(timeout):
+            raise PendingAfterTimeout(f"backend {self.name!r} still has pending work after "
+                                      f"{timeout}s")
+        self.settle(ev)
+        self.state = "finalized"
+        self.comm.destroy()
+
+    # ---------------------------------------------------------------- launch
+    def _launch(self, req: CommRequest, st: _Staging, s: int) -> None:
+        lib, c = self.comm.lib, self.comm.handle
+        kind, p, rank, seq = req.kind, self.world_size, self.rank, req.seq
+        from ..dispatch import message_bytes
+
+        nbytes = message_bytes(req, p)
+        algo = self._algo_code(kind, nbytes)
+        req._algorithm = next((k for k, v in ALGO_CODES.items() if v == algo), "auto")
+        chk = _lib.check
+
+        if kind in (CommOpKind.all_reduce, CommOpKind.reduce, CommOpKind.reduce_scatter):
+            i = st.dev(req.input)
+            dt, op = req.input.dtype, req.op.code
+            if kind is CommOpKind.all_reduce:
+                o = st.dev(req.output, upload=req.output is req.input, download=True)
+                chk(lib.mcrdl_all_reduce(c, _ptr(i), _ptr(o), req.input.count, dt.code, op, algo,
+                                         seq, s))
+            elif kind is CommOpKind.reduce:
+                if rank == req.root:
+                    o = st.dev(req.output, upload=req.output is req.input, download=True)
+                else:
+                    o = st.scratch(req.input.count, dt)
+                chk(lib.mcrdl_all_reduce(c, _ptr(i), _ptr(o), req.input.count, dt.code, op, algo,
+                                         seq, s))
+            else:
+                m = req.output.count
+                full = st.scratch(p * m, dt)
+                chk(lib.mcrdl_all_reduce(c, _ptr(i), _ptr(full), p * m, dt.code, op, algo, seq, s))
+                o = st.dev(req.output, upload=False, download=True)
+                o.copy_(full[rank * m:(rank + 1) * m])
+            return
+
+        if kind is CommOpKind.bcast:
+            b = st.dev(req.output, upload=True, download=True)
+            chk(lib.mcrdl_bcast(c, _ptr(b), req.output.count, req.output.dtype.code, req.root,
+                                algo, seq, s))
+            return
+
+        if kind in (CommOpKind.all_gather, CommOpKind.all_gatherv):
+            i = st.dev(req.input)
+            o = st.dev(req.output, upload=False, download=True)
+            dt = req.input.dtype
+            if kind is CommOpKind.all_gather:
+                n = req.input.count
+                counts, displs = [n] * p, [r * n for r in range(p)]
+            else:
+                counts, displs = req.rcounts, req.rdispls
+            if _is_dev(counts) or _is_dev(displs):
+                sc = counts[rank].reshape(1).expand(p)
+                dc = _dev_counts(st, sc, torch.zeros_like(sc), counts, displs)
+                chk(lib.mcrdl_all_to_allv_dev(c, _ptr(i), i.numel(), _ptr(o), o.numel(), _ptr(dc),
+                                              dt.code, algo, seq, s))
+            else:
+                chk(lib.mcrdl_all_gatherv(c, _ptr(i), _ptr(o), _lib.i64_array(counts),
+                                          _lib.i64_array(displs), dt.code, algo, seq, s))
+            return
+
+        if kind in (CommOpKind.gather, CommOpKind.gatherv):
+            i = st.dev(req.input)
+            o = st.dev(req.output, upload=False, download=True) if req.output is not None else None
+            dt = req.input.dtype
+            if kind is CommOpKind.gather:
+                n = req.input.count
+                counts, displs = [n] * p, [r * n for r in range(p)]
+            else:
+                counts, displs = _host_list(req.rcounts), _host_list(req.rdispls)
+            chk(lib.mcrdl_gatherv(c, _ptr(i), _ptr(o), _lib.i64_array(counts),
+                                  _lib.i64_array(displs), req.root, dt.code, algo, seq, s))
+            return
+
+        if kind in (CommOpKind.scatter, CommOpKind.scatterv):
+            o = st.dev(req.output, upload=False, download=True)
+            i = st.dev(req.input) if req.input is not None else None
+            dt = req.output.dtype
+            if kind is CommOpKind.scatter:
+                n = req.output.count
+                counts, displs = [n] * p, [r * n for r in range(p)]
+            else:
+                counts, displs = _host_list(req.scounts), _host_list(req.sdispls)
+            root = req.root
+            if rank == root:
+                sc, sd = list(counts), list(displs)
+            else:
+                sc, sd = [0] * p, [0] * p
+            rc, rd = [0] * p, [0] * p
+            rc[root] = counts[rank]
+            chk(lib.mcrdl_all_to_allv(c, _ptr(i), _ptr(o), _lib.i64_array(sc), _lib.i64_array(sd),
+                                      _lib.i64_array(rc), _lib.i64_array(rd), dt.code, algo, seq, s))
+            return
+
+        if kind is CommOpKind.all_to_all_single:
+            same = req.input is req.output
+            i = st.dev(req.input)
+            o = i if same else st.dev(req.output, upload=False, download=True)
+            if same:
+                st.dev(req.output, download=True)
+            chk(lib.mcrdl_all_to_all_single(c, _ptr(i), _ptr(o), req.input.count,
+                                            req.input.dtype.code, algo, seq, s))
+            return
+
+        if kind is CommOpKind.all_to_all:
+            ins = [st.dev(b) for b in req.input]
+            outs = [st.dev(b, upload=False, download=True) for b in req.output]
+            chk(lib.mcrdl_all_to_all_ptrs(
+                c, _lib.ptr_array([_ptr(t) for t in ins]),
+                _lib.i64_array([b.count for b in req.input]),
+                _lib.ptr_array([_ptr(t) for t in outs]),
+                _lib.i64_array([b.count for b in req.output]),
+                req.input[0].dtype.code, algo, seq, s))
+            return
+
+        if kind is CommOpKind.all_to_allv:
+            dt = req.input.dtype
+            i = st.dev(req.input)
+            o = st.dev(req.output, upload=False, download=True)
+            vecs = (req.scounts, req.sdispls, req.rcounts, req.rdispls)
+            if any(_is_dev(v) for v in vecs):
+                if i.data_ptr() == o.data_ptr():
+                    i = i.clone()
+                dc = _dev_counts(st, *vecs)
+                chk(lib.mcrdl_all_to_allv_dev(c, _ptr(i), i.numel(), _ptr(o), o.numel(), _ptr(dc),
+                                              dt.code, algo, seq, s))
+                return
+            sc, sd, rc, rd = (list(map(int, v)) for v in vecs)
+            if i.data_ptr() == o.data_ptr() and (sc != rc or sd != rd):
+                i = i.clone()  # the reference snapshots aliased input (collectives.py:662-663)
+            chk(lib.mcrdl_all_to_allv(c, _ptr(i), _ptr(o), _lib.i64_array(sc), _lib.i64_array(sd),
+                                      _lib.i64_array(rc), _lib.i64_array(rd), dt.code, algo, seq, s))
+            return
+
+        raise UnsupportedOperation(f"{kind.name} is not supported by the nvlink backend")
+
+
+def _is_dev(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor)
+
+
+def _host_list(x) -> list:
+    if _is_dev(x):
+        return [int(v) for v in x.tolist()]
+    return [int(v) for v in x]
+
+
+def _dev_counts(st: _Staging, sc, sd, rc, rd):
+    parts = []
+    for v in (sc, sd, rc, rd):
+        if _is_dev(v):
+            parts.append(v.to(device=st.device, dtype=torch.int64).reshape(-1))
+        else:
+            parts.append(torch.tensor([int(x) for x in v], dtype=torch.int64).to(
+                st.device, non_blocking=False))
+    dc = torch.cat(parts).contiguous()
+    st.keep.append(dc)
+    return dc

@@ -1,0 +1,424 @@
+"""One rank of a multi-GPU parity run (launched by tests/test_gpu_parity.py
+and __graft_entry__.smoke via tests/gpu_launch.py). Runs every scenario
+through the public Runtime API on the nvlink backend and checks each rank's
+result against the CPU oracle (oracle/seqref.py) on identically seeded
+inputs. Writes a JSON report {rank, failures, checked, launches}.
+
+Usage: RANK=r WORLD_SIZE=p LOCAL_RANK=r MCRDL_MASTER_PORT=... \
+       python tests/gpu_worker.py <report.json> [scenario,...]
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import traceback
+import zlib
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+import paper_2303_08374_b200 as mc  # noqa: E402
+from paper_2303_08374_b200 import (AlgorithmPolicy, BackendConfig, Buffer, CommOpKind,  # noqa: E402
+                                   CommRequest, DType, FusionConfig, ReduceOp, Runtime)
+from paper_2303_08374_b200.errors import OrderMismatch  # noqa: E402
+from paper_2303_08374_b200.nvl import _lib  # noqa: E402
+from oracle import seqref  # noqa: E402
+
+NP = {DType.f32: np.float32, DType.f64: np.float64, DType.i32: np.int32, DType.i64: np.int64,
+      DType.u8: np.uint8, DType.bf16: np.uint16}
+
+
+def seed_of(*parts) -> int:
+    return zlib.crc32("|".join(str(p) for p in parts).encode())
+
+
+def values(dtype: DType, n: int, *seed) -> np.ndarray:
+    """Seeded inputs (tests/cases.py:32-37): floats normal, ints [-1000,1000),
+    u8 [0,256); bf16 as RNE-rounded normals (uint16 bits)."""
+    rng = np.random.default_rng(seed_of(*seed))
+    if dtype is DType.bf16:
+        return seqref.f32_to_bf16_bits(rng.standard_normal(n).astype(np.float32))
+    if dtype.is_float:
+        return rng.standard_normal(n).astype(NP[dtype])
+    if dtype is DType.u8:
+        return rng.integers(0, 256, size=n).astype(np.uint8)
+    return rng.integers(-1000, 1000, size=n).astype(NP[dtype])
+
+
+def small_prod_values(dtype, n, *seed):
+    rng = np.random.default_rng(seed_of(*seed))
+    if dtype is DType.bf16:
+        return seqref.f32_to_bf16_bits(rng.uniform(0.5, 1.5, n).astype(np.float32))
+    if dtype.is_float:
+        return rng.uniform(0.5, 1.5, n).astype(NP[dtype])
+    return rng.integers(1, 4, size=n).astype(NP[dtype])
+
+
+def to_dev(arr: np.ndarray, dtype: DType, dev) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    if dtype is DType.bf16:
+        t = t.view(torch.bfloat16)
+    return t.to(dev)
+
+
+def from_dev(t: torch.Tensor, dtype: DType) -> np.ndarray:
+    t = t.detach().cpu()
+    if dtype is DType.bf16:
+        return t.view(torch.int16).numpy().view(np.uint16)
+    return t.numpy()
+
+
+class Ctx:
+    def __init__(self, rt: Runtime, backend: str):
+        self.rt = rt
+        self.b = backend
+        self.p = rt.world_size
+        self.r = rt.rank
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.failures = []
+        self.checked = 0
+
+    def check(self, name, got, want, float_reduction=False, rtol=1e-5):
+        self.checked += 1
+        try:
+            seqref.assert_matches(got, want, float_reduction=float_reduction, rtol=rtol, where=name)
+        except AssertionError as exc:
+            msg = str(exc)
+            self.failures.append(f"{name}: {msg[:600]}")
+
+
+# ---------------------------------------------------------------- scenarios
+
+def sc_all_reduce(cx: Ctx):
+    p, r = cx.p, cx.r
+    sizes = [1, 7, 64, 1000, 4097, 65536 + 3, 1 << 20]
+    for algo in ("one_shot", "two_shot"):
+        for dtype in (DType.f32, DType.bf16, DType.i64, DType.i32, DType.f64, DType.u8):
+            for op in ("sum", "prod", "min", "max"):
+                for n in sizes:
+                    if op == "prod" and n > 4097:
+                        continue
+                    gen = small_prod_values if op == "prod" else values
+                    ins = [gen(dtype, n, "ar", algo, dtype.name, op, n, q) for q in range(p)]
+                    if dtype is DType.bf16:
+                        want = seqref.fold_bf16(ins, op)
+                    else:
+                        want = seqref.fold(ins, op)
+                    t = to_dev(ins[r], dtype, cx.dev)
+                    req = CommRequest(CommOpKind.all_reduce, input=Buffer(t), output=Buffer(t),
+                                      op=ReduceOp(op), backend=cx.b)
+                    cx.rt._instance(cx.b).policy = AlgorithmPolicy({CommOpKind.all_reduce: algo})
+                    cx.rt.post(req)
+                    cx.check(f"all_reduce/{algo}/{dtype.name}/{op}/{n}", from_dev(t, dtype), want)
+    cx.rt._instance(cx.b).policy = AlgorithmPolicy()
+    # out-of-place + misaligned (element offset 1 -> scalar path)
+    for dtype in (DType.f32, DType.bf16):
+        n = 10001
+        ins = [values(dtype, n + 1, "arm", dtype.name, q) for q in range(p)]
+        want = (seqref.fold_bf16 if dtype is DType.bf16 else seqref.fold)([x[1:] for x in ins], "sum")
+        src = to_dev(ins[r], dtype, cx.dev)[1:]
+        dst = torch.empty(n + 1, dtype=src.dtype, device=cx.dev)[1:]
+        cx.rt.post(CommRequest(CommOpKind.all_reduce, input=Buffer(src), output=Buffer(dst),
+                               op=ReduceOp.sum, backend=cx.b))
+        cx.check(f"all_reduce/misaligned/{dtype.name}", from_dev(dst, dtype), want)
+    # large two-shot that spans several workspace chunks
+    n = (96 << 20) // 4 + 5
+    ins = [values(DType.f32, n, "arbig", q) for q in range(p)]
+    want = seqref.fold(ins, "sum")
+    t = to_dev(ins[r], DType.f32, cx.dev)
+    cx.rt.all_reduce(cx.b, Buffer(t))
+    cx.check("all_reduce/f32/96MiB", from_dev(t, DType.f32), want)
+
+
+def counts_matrix(p, count, *seed):
+    rng = np.random.default_rng(seed_of(*seed))
+    return [[int(rng.integers(0, count + 1)) for _ in range(p)] for _ in range(p)]
+
+
+def packed(c):
+    out, o = [], 0
+    for x in c:
+        out.append(o)
+        o += x
+    return out
+
+
+def sc_all_to_allv(cx: Ctx):
+    p, r = cx.p, cx.r
+    for dtype in (DType.f32, DType.bf16, DType.i64, DType.u8):
+        for count in (0, 1, 7, 64, 1000, 50000):
+            sc = counts_matrix(p, count, "a2av", dtype.name, count)
+            sd = [packed(row) for row in sc]
+            rd = [packed([sc[j][q] for j in range(p)]) for q in range(p)]
+            ins = [values(dtype, sum(sc[q]), "a2avin", dtype.name, count, q) for q in range(p)]
+            want = seqref.all_to_allv(ins, sc, sd, rd,
+                                      out_counts=[sum(sc[j][q] for j in range(p)) for q in range(p)])
+            rcounts = [sc[j][r] for j in range(p)]
+            i = to_dev(ins[r], dtype, cx.dev)
+            o = torch.zeros(sum(rcounts), dtype=i.dtype, device=cx.dev)
+            cx.rt.all_to_allv(cx.b, Buffer(o), Buffer(i), sc[r], rcounts, sd[r], rd[r])
+            cx.check(f"a2av/{dtype.name}/{count}", from_dev(o, dtype), want[r])
+            # device-resident counts
+            o2 = torch.zeros_like(o)
+            dc = [torch.tensor(v, dtype=torch.int64, device=cx.dev)
+                  for v in (sc[r], rcounts, sd[r], rd[r])]
+            cx.rt.all_to_allv(cx.b, Buffer(o2), Buffer(i), dc[0], dc[1], dc[2], dc[3])
+            cx.check(f"a2av-devcounts/{dtype.name}/{count}", from_dev(o2, dtype), want[r])
+    # cfg1: 1 MiB f32 per rank, skew weights 1:2..p
+    n = 262144
+    w = np.arange(1, p + 1, dtype=np.float64)
+    row = [int(x) for x in np.floor(w / w.sum() * n)]
+    row[-1] += n - sum(row)
+    sc = [list(row) for _ in range(p)]
+    sd = [packed(x) for x in sc]
+    rd = [packed([sc[j][q] for j in range(p)]) for q in range(p)]
+    ins = [values(DType.f32, n, "cfg1", q) for q in range(p)]
+    want = seqref.all_to_allv(ins, sc, sd, rd)
+    rc = [sc[j][r] for j in range(p)]
+    i = to_dev(ins[r], DType.f32, cx.dev)
+    o = torch.zeros(sum(rc), dtype=torch.float32, device=cx.dev)
+    cx.rt.all_to_allv(cx.b, Buffer(o), Buffer(i), sc[r], rc, sd[r], rd[r])
+    cx.check("a2av/cfg1", from_dev(o, DType.f32), want[r])
+
+
+def sc_all_to_all(cx: Ctx):
+    p, r = cx.p, cx.r
+    for m in (0, 1, 5, 4096, 100003):
+        ins = [values(DType.i64, p * m, "a2as", m, q) for q in range(p)]
+        want = seqref.all_to_all_single(ins)
+        i = to_dev(ins[r], DType.i64, cx.dev)
+        o = torch.zeros_like(i)
+        cx.rt.all_to_all_single(cx.b, Buffer(o), Buffer(i))
+        cx.check(f"a2a_single/{m}", from_dev(o, DType.i64), want[r])
+        # in place (the reference snapshots, collectives.py:662-663)
+        io = to_dev(ins[r], DType.i64, cx.dev)
+        bb = Buffer(io)
+        cx.rt.post(CommRequest(CommOpKind.all_to_all_single, input=bb, output=bb, backend=cx.b))
+        cx.check(f"a2a_single/inplace/{m}", from_dev(io, DType.i64), want[r])
+    # list form
+    blocks = [[values(DType.f32, 3 + q + j, "a2al", q, j) for j in range(p)] for q in range(p)]
+    want = seqref.all_to_all(blocks)
+    ins = [Buffer(to_dev(blocks[r][j], DType.f32, cx.dev)) for j in range(p)]
+    outs = [Buffer(torch.zeros(3 + j + r, dtype=torch.float32, device=cx.dev)) for j in range(p)]
+    cx.rt.all_to_all(cx.b, outs, ins)
+    for j in range(p):
+        cx.check(f"a2a_list[{j}]", from_dev(outs[j].array, DType.f32), want[r][j])
+
+
+def sc_gathers(cx: Ctx):
+    p, r = cx.p, cx.r
+    for dtype in (DType.i64, DType.f32, DType.u8):
+        for count in (0, 1, 5, 1000, 70001):
+            rng = np.random.default_rng(seed_of("agv", dtype.name, count))
+            counts = [int(rng.integers(0, count + 1)) for _ in range(p)]
+            if p > 2:
+                counts[1] = 0  # zero-length middle segment (test_collectives.py:84-94)
+            displs = packed(counts)
+            ins = [values(dtype, counts[q], "agvin", dtype.name, count, q) for q in range(p)]
+            want = seqref.all_gatherv(ins, counts, displs)
+            i = to_dev(ins[r], dtype, cx.dev)
+            o = torch.zeros(sum(counts), dtype=i.dtype, device=cx.dev)
+            cx.rt.all_gatherv(cx.b, Buffer(o), Buffer(i), counts, displs)
+            cx.check(f"allgatherv/{dtype.name}/{count}", from_dev(o, dtype), want[r])
+            for root in range(p):
+                o = torch.zeros(sum(counts), dtype=i.dtype, device=cx.dev) if r == root else None
+                cx.rt.gatherv(cx.b, Buffer(o) if o is not None else None, Buffer(i), root, counts,
+                              displs)
+                if r == root:
+                    cx.check(f"gatherv/{dtype.name}/{count}/root{root}", from_dev(o, dtype),
+                             seqref.gatherv(ins, root, counts, displs)[root])
+        n = 333
+        ins = [values(dtype, n, "ag", dtype.name, q) for q in range(p)]
+        i = to_dev(ins[r], dtype, cx.dev)
+        o = torch.zeros(p * n, dtype=i.dtype, device=cx.dev)
+        cx.rt.all_gather(cx.b, Buffer(o), Buffer(i))
+        cx.check(f"allgather/{dtype.name}", from_dev(o, dtype), seqref.all_gather(ins)[r])
+        root = p - 1
+        o = torch.zeros(p * n, dtype=i.dtype, device=cx.dev) if r == root else None
+        cx.rt.gather(cx.b, Buffer(o) if o is not None else None, Buffer(i), root)
+        if r == root:
+            cx.check(f"gather/{dtype.name}", from_dev(o, dtype), seqref.gather(ins, root)[root])
+
+
+def sc_bcast_scatter(cx: Ctx):
+    p, r = cx.p, cx.r
+    for dtype, n in ((DType.u8, 65536), (DType.f32, 1), (DType.i32, 12345), (DType.bf16, 4096)):
+        for root in range(p):
+            ins = [values(dtype, n, "bc", dtype.name, root, q) for q in range(p)]
+            t = to_dev(ins[r], dtype, cx.dev)
+            cx.rt.bcast(cx.b, Buffer(t), root)
+            cx.check(f"bcast/{dtype.name}/root{root}", from_dev(t, dtype), ins[root])
+    for root in range(p):
+        m = 777
+        src = values(DType.f32, p * m, "sc", root)
+        o = torch.zeros(m, dtype=torch.float32, device=cx.dev)
+        i = Buffer(to_dev(src, DType.f32, cx.dev)) if r == root else None
+        cx.rt.scatter(cx.b, Buffer(o), i, root)
+        cx.check(f"scatter/root{root}", from_dev(o, DType.f32), seqref.scatter(src, p)[r])
+        counts = [(q * 7 + 3) % 11 for q in range(p)]
+        displs = packed(counts)
+        src = values(DType.i64, sum(counts), "scv", root)
+        o = torch.zeros(counts[r], dtype=torch.int64, device=cx.dev)
+        i = Buffer(to_dev(src, DType.i64, cx.dev)) if r == root else None
+        cx.rt.scatterv(cx.b, Buffer(o), i, root, counts, displs)
+        cx.check(f"scatterv/root{root}", from_dev(o, DType.i64),
+                 seqref.scatterv(src, counts, displs)[r])
+
+
+def sc_reduce_family(cx: Ctx):
+    p, r = cx.p, cx.r
+    n = 5000
+    for root in range(p):
+        ins = [values(DType.f32, n, "red", root, q) for q in range(p)]
+        t = to_dev(ins[r], DType.f32, cx.dev)
+        cx.rt.reduce(cx.b, Buffer(t), root, ReduceOp.sum)
+        if r == root:
+            cx.check(f"reduce/root{root}", from_dev(t, DType.f32), seqref.fold(ins, "sum"))
+        else:
+            cx.check(f"reduce/nonroot-untouched/{root}", from_dev(t, DType.f32), ins[r])
+    m = 1001
+    ins = [values(DType.i64, p * m, "rs", q) for q in range(p)]
+    o = torch.zeros(m, dtype=torch.int64, device=cx.dev)
+    cx.rt.reduce_scatter(cx.b, Buffer(o), Buffer(to_dev(ins[r], DType.i64, cx.dev)))
+    cx.check("reduce_scatter", from_dev(o, DType.i64), seqref.reduce_scatter(ins, "sum")[r])
+
+
+def sc_host_buffers(cx: Ctx):
+    """Reference-style numpy Buffers through the device backend (staged)."""
+    p, r = cx.p, cx.r
+    ins = [values(DType.f32, 4099, "host", q) for q in range(p)]
+    b = Buffer(ins[r].copy())
+    cx.rt.all_reduce(cx.b, b)
+    cx.check("host/all_reduce", b.array, seqref.fold(ins, "sum"))
+    # partner.py known answers (p=2 world, frontend/test/helpers/partner.py:60-159)
+    if p == 2:
+        buf = Buffer.from_values(DType.i64, [r + 1, 10 * (r + 1)])
+        cx.rt.all_reduce(cx.b, buf)
+        cx.check("known/allreduce_i64", buf.array, np.array([3, 30], dtype=np.int64))
+        buf = Buffer.from_values(DType.f32, [0.5 + r, 2.5 * (r + 1)])
+        cx.rt.all_reduce(cx.b, buf)
+        cx.check("known/allreduce_f32", buf.array, np.array([2.0, 7.5], dtype=np.float32))
+        sc = [[1, 2], [2, 1]]
+        inp = Buffer.from_values(DType.i64, [[1, 2, 3], [4, 5, 6]][r])
+        rc = [sc[j][r] for j in range(p)]
+        out = Buffer.zeros(DType.i64, sum(rc))
+        cx.rt.all_to_allv(cx.b, out, inp, sc[r], rc, [0, sc[r][0]], [0, rc[0]])
+        cx.check("known/alltoallv", out.array, np.array([[1, 4, 5], [2, 3, 6]][r], dtype=np.int64))
+        inp = Buffer.from_values(DType.i64, [[1, 2], [3, 4]][r])
+        out = Buffer.zeros(DType.i64, 2)
+        cx.rt.all_to_all_single(cx.b, out, inp)
+        cx.check("known/a2a_single", out.array, np.array([[1, 3], [2, 4]][r], dtype=np.int64))
+        inp = Buffer.from_values(DType.i64, [11, 12] if r == 0 else [21])
+        gout = Buffer.zeros(DType.i64, 3) if r == 1 else None
+        cx.rt.gatherv(cx.b, gout, inp, 1, [2, 1], [0, 2])
+        if r == 1:
+            cx.check("known/gatherv", gout.array, np.array([11, 12, 21], dtype=np.int64))
+        buf = Buffer.from_values(DType.f32, [3.25, -1.5]) if r == 0 else Buffer.zeros(DType.f32, 2)
+        cx.rt.bcast(cx.b, buf, 0)
+        cx.check("known/bcast", buf.array, np.array([3.25, -1.5], dtype=np.float32))
+
+
+def sc_async_and_fusion(cx: Ctx):
+    p, r = cx.p, cx.r
+    # 14 DLRM MLP gradients through fusion, posted async
+    shapes = [6656, 512, 262144, 512, 65536, 128, 490496, 1024, 1048576, 1024, 1048576, 1024,
+              1024, 1]
+    ins = [[values(DType.f32, n, "fus", k, q) for q in range(p)] for k, n in enumerate(shapes)]
+    ts = [to_dev(ins[k][r], DType.f32, cx.dev) for k in range(len(shapes))]
+    hs = [cx.rt.all_reduce("fused", Buffer(t), ReduceOp.sum, async_op=True) for t in ts]
+    for h in hs:
+        cx.rt.wait(h)
+    torch.cuda.synchronize()
+    for k, t in enumerate(ts):
+        cx.check(f"fusion/{k}/{shapes[k]}", from_dev(t, DType.f32), seqref.fold(ins[k], "sum"))
+    # async handles on the plain backend + synchronize
+    xs = [values(DType.i32, 10000 + k, "async", k, q) for k in range(6) for q in range(p)]
+    ts = [to_dev(xs[k * p + r], DType.i32, cx.dev) for k in range(6)]
+    hs = [cx.rt.all_reduce(cx.b, Buffer(t), async_op=True) for t in ts]
+    cx.rt.synchronize([cx.b])
+    for k, h in enumerate(hs):
+        assert h.test()
+        cx.check(f"async/{k}", from_dev(ts[k], DType.i32),
+                 seqref.fold([xs[k * p + q] for q in range(p)], "sum"))
+
+
+def sc_order_mismatch(cx: Ctx):
+    """Ranks post different ops at the same seq -> OrderMismatch everywhere
+    (test_acceptance.py:214-243, collectives.py:283-285)."""
+    if cx.p < 2:
+        return
+    n = 1000 + (7 if cx.r == 0 else 0)
+    t = torch.ones(n, dtype=torch.float32, device=cx.dev)
+    cx.rt.all_reduce("mism", Buffer(t), async_op=True)
+    raised = None
+    try:
+        cx.rt.synchronize(["mism"])
+    except OrderMismatch as exc:
+        raised = exc
+    except Exception as exc:  # noqa: BLE001
+        raised = exc
+    cx.checked += 1
+    if not isinstance(raised, OrderMismatch):
+        cx.failures.append(f"order_mismatch: expected OrderMismatch, got {raised!r}")
+
+
+SCENARIOS = {
+    "all_reduce": sc_all_reduce,
+    "all_to_allv": sc_all_to_allv,
+    "all_to_all": sc_all_to_all,
+    "gathers": sc_gathers,
+    "bcast_scatter": sc_bcast_scatter,
+    "reduce_family": sc_reduce_family,
+    "host_buffers": sc_host_buffers,
+    "async_fusion": sc_async_and_fusion,
+    "order_mismatch": sc_order_mismatch,
+}
+
+
+def main() -> int:
+    report = sys.argv[1]
+    names = sys.argv[2].split(",") if len(sys.argv) > 2 else list(SCENARIOS)
+    rank = int(os.environ["RANK"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    out = {"rank": rank, "failures": [], "checked": 0}
+    rt = Runtime()
+    try:
+        cfgs = [BackendConfig("nvl"), BackendConfig("fused", fusion=FusionConfig(max_bytes=1 << 20,
+                                                                               max_wait=5.0))]
+        if "order_mismatch" in names:
+            cfgs.append(BackendConfig("mism", workspace_bytes=8 << 20))
+        rt.init(cfgs)
+        cx = Ctx(rt, "nvl")
+        for name in names:
+            try:
+                SCENARIOS[name](cx)
+            except Exception:  # noqa: BLE001
+                cx.failures.append(f"{name}: exception\n{traceback.format_exc()[-3000:]}")
+        torch.cuda.synchronize()
+        try:
+            rt.synchronize(["nvl", "fused"])
+        except Exception as exc:  # noqa: BLE001
+            cx.failures.append(f"synchronize: {exc!r}")
+        out["failures"] = cx.failures
+        out["checked"] = cx.checked
+        out["launches"] = _lib.launch_count()
+    except Exception:  # noqa: BLE001
+        out["failures"].append("init/run: " + traceback.format_exc()[-3000:])
+    finally:
+        Path(report).write_text(json.dumps(out))
+        try:
+            rt.close()
+        except Exception:  # noqa: BLE001
+            pass
+    return 0 if not out["failures"] else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
