@@ -67,91 +67,172 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// ----------------------------------------------------------------- two-shot
-// Segment j = packs [j*sp, (j+1)*sp) (sp = ceil(npk / p)); block b owns the
-// same sub-range [b*sp/G, (b+1)*sp/G) of every segment.
-//   RS: push my copy of segment j to rank j (RS area, slot `rank`); flag.
-//   fold: segment `rank` = ascending fold of the p slots -> out + every
-//         peer's AG area (slot `rank`); flag2.
-//   AG: copy AG slots r != rank into out.
-// Workspace per half: RS area p*segb + AG area p*segb.
+// ------------------------------------------------ pipelined two-shot (K2)
+// Three CTA roles run concurrently over the same share s of every segment,
+// handing off 64 KiB chunks through per-chunk release flags:
+//   senders   [0, gp)     RS push: my copy of segment q, chunk r -> rank q
+//   reducers  [gp, 2gp)   fold chunk r of my segment (ascending ranks) ->
+//                         out + every peer's AG area
+//   gatherers [2gp, 3gp)  land every peer's reduced chunk r into out
+// NVLink carries RS and AG traffic at the same time and local HBM work hides
+// under it. Senders never wait; reducers wait only for senders; gatherers
+// only for reducers: progress does not need CTA co-residency.
+template <typename T, bool VEC>
+__device__ __forceinline__ void push_packs(const T* in, int64_t n, int64_t g0, int64_t cnt,
+                                           uint8_t* dst) {
+  // packs [g0, g0+cnt) of `in` -> dst (16-byte aligned, pack i at dst + 16*(i-g0))
+  const int tid = threadIdx.x, nt = blockDim.x;
+  int64_t i = tid;
+  for (; i + 3 * nt < cnt; i += 4 * nt) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = load_pack<T, VEC>(in, g0 + i + u * nt, n);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) st16(dst + (i + u * nt) * 16, v[u]);
+  }
+  for (; i < cnt; i += nt) st16(dst + i * 16, load_pack<T, VEC>(in, g0 + i, n));
+}
+
+__device__ __forceinline__ int64_t seg_len(int64_t npk, int64_t sp, int q, int64_t rb, int64_t re) {
+  // packs of share [rb, re) that exist in segment q
+  const int64_t hi = min(re, npk - int64_t(q) * sp);
+  return hi > rb ? hi - rb : 0;
+}
+__device__ __forceinline__ int nchunks(int64_t len, int64_t chp, int s) {
+  int k = int((len + chp - 1) / chp);
+  return (k == 0 && s == 0) ? 1 : k;  // share 0 always carries a flag (order check)
+}
+
 template <typename T, int OP, bool VEC>
-__global__ void __launch_bounds__(kThreads)
-    k_ar_twoshot(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb,
-                 uint32_t epoch, uint32_t sig) {
+__global__ void __launch_bounds__(kThreads, 2)
+    k_ar_pipe(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp,
+              int64_t chp, uint32_t epoch, uint32_t sig) {
   constexpr int N = Pack<T>::N;
   __shared__ int s_err;
   __shared__ SComm S;
   const int par = epoch & 1, rank = c.rank, world = c.world;
-  const int b = blockIdx.x, G = gridDim.x, tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int role = int(blockIdx.x) / gp, s = int(blockIdx.x) % gp;
   const int64_t npk = (n + N - 1) / N;
-  const int64_t rb = sp * b / G, re = sp * (b + 1) / G;  // sub-range within a segment
+  const int64_t rb = sp * s / gp, re = sp * (s + 1) / gp;
   const int64_t hoff = int64_t(par) * c.half_bytes;
   const int64_t ag = int64_t(world) * segb;
   if (tid == 0) s_err = 0;
   stage_comm(c, S);
   __syncthreads();
-
-  // ---- RS push: for each sub-range pack, send segment j's copy to rank j.
-  for (int64_t i = rb + tid; i < re; i += nt) {
-    for (int k = 1; k < world; ++k) {
-      const int q = (rank + k) % world;
-      const int64_t gi = int64_t(q) * sp + i;
-      if (gi >= npk) continue;
-      const uint4 v = load_pack<T, VEC>(in, gi, n);
-      st16(S.ws[q] + hoff + int64_t(rank) * segb + i * 16, v);
-    }
-  }
-  __syncthreads();
-  if (tid < world && tid != rank) publish(&S.pad[tid]->flag[par][b][rank], make_flag(epoch, sig, 0));
-  if (tid < world && tid != rank) {
-    int e = wait_flag(&S.pad[rank]->flag[par][b][tid], S.pad[rank], c.timeout_ns, epoch, sig, 0);
-    if (e) atomicCAS(&s_err, 0, e);
-  }
-  __syncthreads();
-  if (s_err) {
-    if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
-    return;
-  }
-
-  // ---- fold my segment, scatter the result to every peer's AG area.
   const uint8_t* ws = S.ws[rank] + hoff;
-  for (int64_t i = rb + tid; i < re; i += nt) {
-    const int64_t gi = int64_t(rank) * sp + i;
-    if (gi >= npk) break;
-    Pack<T> acc;
-    acc.from_raw(rank == 0 ? load_pack<T, VEC>(in, gi, n) : ld16_cg(ws + i * 16));
-    for (int r = 1; r < world; ++r) {
-      const uint4 v = (r == rank) ? load_pack<T, VEC>(in, gi, n)
-                                  : ld16_cg(ws + int64_t(r) * segb + i * 16);
-      acc.template fold<OP>(v);
+
+  if (role == 0) {  // ---------------------------------------------- sender
+    int rows = 0;
+    for (int q = 0; q < world; ++q)
+      if (q != rank) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
+    for (int r = 0; r < rows; ++r) {
+      for (int k = 1; k < world; ++k) {
+        const int q = (rank + k) % world;
+        const int64_t len = seg_len(npk, sp, q, rb, re);
+        const int64_t lo = int64_t(r) * chp;
+        if (lo >= len) continue;
+        const int64_t cnt = min(chp, len - lo);
+        push_packs<T, VEC>(in, n, int64_t(q) * sp + rb + lo, cnt,
+                           S.ws[q] + hoff + int64_t(rank) * segb + (rb + lo) * 16);
+      }
+      __syncthreads();
+      if (tid < world && tid != rank && r < nchunks(seg_len(npk, sp, tid, rb, re), chp, s))
+        publish(&S.pad[tid]->flag[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
     }
-    const uint4 res = acc.to_raw();
-    for (int k = 1; k < world; ++k) {
-      const int q = (rank + k) % world;
-      st16(S.ws[q] + hoff + ag + int64_t(rank) * segb + i * 16, res);
-    }
-    store_pack<T, VEC>(out, gi, n, res);
-  }
-  __syncthreads();
-  if (tid < world && tid != rank) publish(&S.pad[tid]->flag2[par][b][rank], make_flag(epoch, sig, 1));
-  if (tid < world && tid != rank) {
-    int e = wait_flag(&S.pad[rank]->flag2[par][b][tid], S.pad[rank], c.timeout_ns, epoch, sig, 1);
-    if (e) atomicCAS(&s_err, 0, e);
-  }
-  __syncthreads();
-  if (s_err) {
-    if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
     return;
   }
 
-  // ---- AG: land every other rank's reduced segment in `out`.
-  for (int64_t i = rb + tid; i < re; i += nt) {
+  if (role == 1) {  // --------------------------------------------- reducer
+    const int64_t len = seg_len(npk, sp, rank, rb, re);
+    const int rows = nchunks(len, chp, s);
+    for (int r = 0; r < rows; ++r) {
+      if (tid < world && tid != rank) {
+        int e = wait_flag(&S.pad[rank]->flag[par][s][tid], S.pad[rank], c.timeout_ns, epoch, sig,
+                          uint32_t(r + 1));
+        if (e) atomicCAS(&s_err, 0, e);
+      }
+      __syncthreads();
+      if (s_err) {
+        if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+        return;
+      }
+      const int64_t lo = int64_t(r) * chp, hi = min(len, lo + chp);
+      // RU packs per thread in flight: each rank's RU loads issue before the fold.
+      constexpr int RU = sizeof(T) == 2 ? 2 : 4;
+      int64_t i0 = rb + lo + tid;
+      for (; i0 < rb + hi; i0 += RU * nt) {
+        Pack<T> acc[RU];
+        uint4 v[RU];
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const int64_t i = i0 + u * nt;
+          if (i < rb + hi)
+            v[u] = rank == 0 ? load_pack<T, VEC>(in, int64_t(rank) * sp + i, n) : ld16_cg(ws + i * 16);
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) acc[u].from_raw(v[u]);
+        for (int q = 1; q < world; ++q) {
+#pragma unroll
+          for (int u = 0; u < RU; ++u) {
+            const int64_t i = i0 + u * nt;
+            if (i < rb + hi)
+              v[u] = (q == rank) ? load_pack<T, VEC>(in, int64_t(rank) * sp + i, n)
+                                 : ld16_cg(ws + int64_t(q) * segb + i * 16);
+          }
+#pragma unroll
+          for (int u = 0; u < RU; ++u) acc[u].template fold<OP>(v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const int64_t i = i0 + u * nt;
+          if (i >= rb + hi) break;
+          const uint4 res = acc[u].to_raw();
+          for (int k = 1; k < world; ++k) {
+            const int q = (rank + k) % world;
+            st16(S.ws[q] + hoff + ag + int64_t(rank) * segb + i * 16, res);
+          }
+          store_pack<T, VEC>(out, int64_t(rank) * sp + i, n, res);
+        }
+      }
+      __syncthreads();
+      if (tid < world && tid != rank)
+        publish(&S.pad[tid]->flag2[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------- gatherer
+  int rows = 0;
+  for (int q = 0; q < world; ++q)
+    if (q != rank) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
+  for (int r = 0; r < rows; ++r) {
+    if (tid < world && tid != rank && r < nchunks(seg_len(npk, sp, tid, rb, re), chp, s)) {
+      int e = wait_flag(&S.pad[rank]->flag2[par][s][tid], S.pad[rank], c.timeout_ns, epoch, sig,
+                        uint32_t(r + 1));
+      if (e) atomicCAS(&s_err, 0, e);
+    }
+    __syncthreads();
+    if (s_err) {
+      if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+      return;
+    }
     for (int k = 1; k < world; ++k) {
-      const int r = (rank + k) % world;
-      const int64_t gi = int64_t(r) * sp + i;
-      if (gi >= npk) continue;
-      store_pack<T, VEC>(out, gi, n, ld16_cg(ws + ag + int64_t(r) * segb + i * 16));
+      const int q = (rank + k) % world;
+      const int64_t len = seg_len(npk, sp, q, rb, re);
+      const int64_t lo = int64_t(r) * chp;
+      if (lo >= len) continue;
+      const int64_t hi = min(len, lo + chp);
+      const uint8_t* src = ws + ag + int64_t(q) * segb;
+      int64_t i = rb + lo + tid;
+      for (; i + 3 * nt < rb + hi; i += 4 * nt) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ld16_cg(src + (i + u * nt) * 16);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) store_pack<T, VEC>(out, int64_t(q) * sp + i + u * nt, n, v[u]);
+      }
+      for (; i < rb + hi; i += nt) store_pack<T, VEC>(out, int64_t(q) * sp + i, n, ld16_cg(src + i * 16));
     }
   }
 }
@@ -302,7 +383,7 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
   do {
     const int64_t m = (n - done < chunk_elems) ? (n - done) : chunk_elems;
     uint32_t epoch;
-    mcrdl_status_t st = begin_op(c, &epoch);
+    mcrdl_status_t st = begin_op(c, stream, &epoch);
     if (st != MCRDL_OK) return st;
     const uint32_t sig = op_sig(kKindAllReduce, dt, OP, sub, uint64_t(m), seq);
     const T* ip = in + done;
@@ -318,11 +399,20 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
     } else {
       const int64_t sp = (npk + world - 1) / world;
       const int64_t segb = (sp * 16 + 255) / 256 * 256;
-      const int G = grid_for(sp, c->num_sms, 2 * c->num_sms);
+      // CTAs per role: one per 32 KiB of segment; 3 roles x gp <= 2 CTAs/SM.
+      int64_t gp = (sp * 16 + (32 << 10) - 1) / (32 << 10);
+      const int64_t gmax = 2 * c->num_sms / 3 > 0 ? 2 * c->num_sms / 3 : 1;
+      gp = gp < 1 ? 1 : (gp > gmax ? gmax : gp);
+      const int64_t share = (sp + gp - 1) / gp;
+      int64_t chp = (share + 3999) / 4000;  // <= 4000 chunks per share (12-bit flag step)
+      if (chp < 16384) chp = 16384;         // 256 KiB chunks
+      const int G = int(3 * gp);
       if (vec)
-        k_ar_twoshot<T, OP, true><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, epoch, sig);
+        k_ar_pipe<T, OP, true><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, int(gp), chp,
+                                                           epoch, sig);
       else
-        k_ar_twoshot<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, epoch, sig);
+        k_ar_pipe<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, int(gp), chp,
+                                                            epoch, sig);
     }
     count_launch();
     MCRDL_CUDA_CHECK(cudaGetLastError());
@@ -352,7 +442,7 @@ static mcrdl_status_t fused_typed(mcrdl_comm* c, const void* const* in_ptrs, voi
                                   int64_t total, uint64_t seq, int dt, cudaStream_t stream) {
   constexpr int N = Pack<T>::N;
   uint32_t epoch;
-  mcrdl_status_t st = begin_op(c, &epoch);
+  mcrdl_status_t st = begin_op(c, stream, &epoch);
   if (st != MCRDL_OK) return st;
   const int64_t npk = (total + N - 1) / N;
   const int64_t slot = (npk * 16 + 255) / 256 * 256;

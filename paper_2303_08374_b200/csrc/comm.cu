@@ -326,7 +326,7 @@ static mcrdl_status_t alloc_region(mcrdl_comm* c, uint64_t bytes, Region* rg) {
   return MCRDL_OK;
 }
 
-mcrdl_status_t begin_op(mcrdl_comm* comm, uint32_t* epoch) {
+mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, uint32_t* epoch) {
   if (comm == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   if (comm->sticky != MCRDL_OK)
     return set_error(comm->sticky, "communicator poisoned by an earlier device error (%s)",
@@ -336,6 +336,12 @@ mcrdl_status_t begin_op(mcrdl_comm* comm, uint32_t* epoch) {
     return set_error(comm->sticky, "communicator poisoned by an earlier device error (%s)",
                      mcrdl_status_kind(comm->sticky));
   }
+  if (comm->have_last && comm->last_stream != stream) {
+    MCRDL_CUDA_CHECK(cudaEventRecord(comm->order_ev, comm->last_stream));
+    MCRDL_CUDA_CHECK(cudaStreamWaitEvent(stream, comm->order_ev, 0));
+  }
+  comm->last_stream = stream;
+  comm->have_last = true;
   comm->epoch += 1;
   if (comm->epoch == 0) comm->epoch = 1;
   *epoch = comm->epoch;
@@ -434,6 +440,7 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
                                  cudaHostAllocMapped | cudaHostAllocPortable));
   *c->err_host = 0;
   MCRDL_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
+  MCRDL_CUDA_CHECK(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
 
   c->dc.rank = rank;
   c->dc.world = world;
@@ -458,6 +465,7 @@ mcrdl_status_t mcrdl_comm_destroy(mcrdl_comm* c) {
   c->symm.clear();
   unmap_region(c, c->base);
   if (c->err_host) cudaFreeHost(c->err_host);
+  if (c->order_ev) cudaEventDestroy(c->order_ev);
   if (c->listen_fd >= 0) close(c->listen_fd);
   delete c;
   return MCRDL_OK;

@@ -1,6 +1,6 @@
 // Direct-write exchange engine: alltoall(v) (K5), allgatherv (K6), gatherv
-// (K7), bcast (K8, push variant) and the 0-byte barrier, all as one kernel
-// over per-peer (pointer, bytes) spans.
+// (K7), scatter(v), bcast (K8, push variant) and the 0-byte barrier — one
+// kernel over per-peer (pointer, bytes) spans.
 //
 // Reference algorithms being replaced (collectives.py):
 //   _alltoall_pairwise/_naive/_bruck + _BlockView   :648-733
@@ -9,13 +9,19 @@
 //   _bcast_linear/_binomial                          :418-443
 //   pairwise count cross-check in _cross_check       :229-241
 // NVSwitch gives every pair full bandwidth, so there is no ring/tree
-// schedule: every rank writes its chunk for peer j straight into j's
-// workspace slot `rank` over NVLink, raises one flag per (block, pair), and
-// the receiver lands the slot into its output. Pairs larger than a slot move
-// in rounds, the receiver acknowledging each round (bounded workspace, any
-// message size). Counts may live in device memory (MoE routing) and are
-// read by the kernel itself.
+// schedule. The grid is split into two roles that run concurrently:
+//   sender CTAs   [0, Gp)    push share s of every outgoing pair into the
+//                            peer's workspace slot `rank`, one release flag
+//                            per 64 KiB chunk;
+//   receiver CTAs [Gp, 2Gp)  copy their share of the local segment, then land
+//                            each incoming chunk as soon as its flag arrives.
+// So the NVLink push, the local copy and the copy-out overlap; senders never
+// wait except for slot reuse (pairs larger than a workspace slot move in
+// rounds the receiver acknowledges), so forward progress does not depend on
+// CTA co-residency. Pairs agree on their geometry from their own byte count
+// (sender: scount, receiver: rcount) — no extra exchange.
 #include <algorithm>
+#include <cstring>
 
 #include "internal.h"
 
@@ -29,45 +35,65 @@ struct XArgs {
   const int64_t* d_counts;  // [scounts | sdispls | rcounts | rdispls] in elements, or null
   const uint8_t* in_base;
   uint8_t* out_base;
-  int64_t in_count;   // element capacity of in/out (device-count bounds check)
+  int64_t in_count;  // element capacity of in/out (device-count bounds check)
   int64_t out_count;
-  int64_t slot;
+  int64_t slot;      // workspace bytes per (sender) slot per round
   int esize;
-  int gmax;
+  int gmax;          // communicator-wide cap on CTAs per pair
+  int gp;            // CTAs per role in this launch
   uint32_t sig_base;
 };
 
-constexpr int64_t kPairCtaBytes = 64 << 10;  // one CTA per 64 KiB of a pair
+constexpr int64_t kPairCtaBytes = 32 << 10;   // one CTA per 32 KiB of a pair
+constexpr int64_t kChunkBytes = 256 << 10;    // flag granularity inside a share
+constexpr int64_t kMaxSteps = 4000;           // < 4096 (12-bit flag step)
 
-__device__ __forceinline__ int64_t rounds_for(int64_t bytes, int64_t slot) {
+__device__ __host__ __forceinline__ int64_t rounds_for(int64_t bytes, int64_t slot) {
   return bytes <= slot ? 1 : (bytes + slot - 1) / slot;
 }
 __device__ __forceinline__ uint32_t pair_sig(uint32_t base, int64_t bytes) {
   return mix32(base, uint64_t(bytes)) & 0xFFFFFu;
 }
-
-// CTAs that serve one pair: a function of the pair's byte count only, so the
-// sender (which knows its scount) and the receiver (its rcount) partition the
-// pair identically without exchanging anything. Capped by gmax, a
-// communicator-wide constant.
+// CTAs serving one pair: a function of the pair's byte count only.
 __device__ __host__ __forceinline__ int pair_ctas(int64_t bytes, int gmax) {
   int64_t g = (bytes + kPairCtaBytes - 1) / kPairCtaBytes;
-  if (g < 1) g = 1;
-  if (g > gmax) g = gmax;
-  return int(g);
+  return int(g < 1 ? 1 : (g > gmax ? gmax : g));
+}
+__device__ __forceinline__ int64_t pair_chunk(int64_t bytes, int g) {
+  int64_t per = (bytes + g - 1) / g;
+  int64_t ch = (per + kMaxSteps - 1) / kMaxSteps;
+  ch = (ch + 15) & ~int64_t(15);
+  return ch > kChunkBytes ? ch : kChunkBytes;
 }
 
-__global__ void __launch_bounds__(kThreads) k_exchange(DevComm c, XArgs a, uint32_t epoch) {
+// Share s of round t of a pair moving B bytes: [a, e) relative to the round,
+// in n chunks of `ch` bytes. A 0-byte pair still carries one empty chunk on
+// share 0 (its flag is the order check / barrier).
+struct Span {
+  int64_t a, e;
+  int n;
+};
+__device__ __forceinline__ Span span_of(int64_t B, int64_t slot, int g, int64_t ch, int64_t t, int s) {
+  Span sp{0, 0, 0};
+  if (s >= g || t >= rounds_for(B, slot)) return sp;
+  const int64_t len = min(slot, B - t * slot);
+  byte_share(len, s, g, sp.a, sp.e);
+  sp.n = int((sp.e - sp.a + ch - 1) / ch);
+  if (B == 0 && s == 0 && t == 0) sp.n = 1;
+  return sp;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a, uint32_t epoch) {
   __shared__ const uint8_t* s_sp[kMaxRanks];
   __shared__ uint8_t* s_rp[kMaxRanks];
   __shared__ int64_t s_sb[kMaxRanks];
   __shared__ int64_t s_rb[kMaxRanks];
-  __shared__ int s_gs[kMaxRanks];
-  __shared__ int s_gr[kMaxRanks];
   __shared__ int s_err;
   __shared__ SComm S;
   const int par = epoch & 1, rank = c.rank, world = c.world;
-  const int b = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
+  const int tid = threadIdx.x;
+  const bool sender = int(blockIdx.x) < a.gp;
+  const int s = sender ? int(blockIdx.x) : int(blockIdx.x) - a.gp;  // share index
   const int64_t hoff = int64_t(par) * c.half_bytes;
   const int64_t slot = a.slot;
   if (tid == 0) s_err = 0;
@@ -80,8 +106,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange(DevComm c, XArgs a, uint3
       s_sb[tid] = sc * a.esize;
       s_rp[tid] = a.out_base + rd * a.esize;
       s_rb[tid] = rc * a.esize;
-      if (sc < 0 || sd < 0 || rc < 0 || rd < 0 || (sd + sc) > a.in_count ||
-          (rd + rc) > a.out_count)
+      if (sc < 0 || sd < 0 || rc < 0 || rd < 0 || sd + sc > a.in_count || rd + rc > a.out_count)
         s_err = MCRDL_ERR_VALIDATION;
     } else {
       s_sp[tid] = a.sptr[tid];
@@ -89,8 +114,6 @@ __global__ void __launch_bounds__(kThreads) k_exchange(DevComm c, XArgs a, uint3
       s_rp[tid] = a.rptr[tid];
       s_rb[tid] = a.rbytes[tid];
     }
-    s_gs[tid] = pair_ctas(s_sb[tid], a.gmax);
-    s_gr[tid] = pair_ctas(s_rb[tid], a.gmax);
   }
   __syncthreads();
   if (tid == 0 && s_sb[rank] != s_rb[rank]) s_err = MCRDL_ERR_VALIDATION;
@@ -100,76 +123,115 @@ __global__ void __launch_bounds__(kThreads) k_exchange(DevComm c, XArgs a, uint3
     return;
   }
 
-  // Rounds this CTA takes part in (block-uniform).
+  // Per-peer state lives in thread `peer` (tid < world) and is mirrored by
+  // every thread from shared memory when computing block-uniform loop bounds.
+  const int me = tid;  // peer index handled by this thread in flag duties
+  if (sender) {
+    int64_t rmax = 0;
+    for (int j = 0; j < world; ++j)
+      if (j != rank && s < pair_ctas(s_sb[j], a.gmax)) rmax = max(rmax, rounds_for(s_sb[j], slot));
+    int sent = 0;  // chunks published to peer `me` (thread-local, tid < world)
+    for (int64_t t = 0; t < rmax; ++t) {
+      if (t > 0) {  // slot reuse: receiver share s consumed round t-1
+        if (me < world && me != rank) {
+          const int g = pair_ctas(s_sb[me], a.gmax);
+          if (s < g && t < rounds_for(s_sb[me], slot)) {
+            int e = wait_flag(&S.pad[rank]->ack[par][s][me], S.pad[rank], c.timeout_ns, epoch,
+                              pair_sig(a.sig_base, s_sb[me]), uint32_t(t));
+            if (e) atomicCAS(&s_err, 0, e);
+          }
+        }
+        __syncthreads();
+        if (s_err) {
+          if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+          return;
+        }
+      }
+      int rows = 0;
+      for (int j = 0; j < world; ++j) {
+        if (j == rank) continue;
+        const int g = pair_ctas(s_sb[j], a.gmax);
+        rows = max(rows, span_of(s_sb[j], slot, g, pair_chunk(s_sb[j], g), t, s).n);
+      }
+      for (int r = 0; r < rows; ++r) {
+        for (int k = 1; k < world; ++k) {
+          const int j = (rank + k) % world;
+          const int g = pair_ctas(s_sb[j], a.gmax);
+          const int64_t ch = pair_chunk(s_sb[j], g);
+          const Span sp = span_of(s_sb[j], slot, g, ch, t, s);
+          if (r >= sp.n) continue;
+          const int64_t lo = sp.a + r * ch, hi = min(sp.e, lo + ch);
+          block_copy<4>(S.ws[j] + hoff + int64_t(rank) * slot + lo, s_sp[j] + t * slot + lo, hi - lo);
+        }
+        __syncthreads();
+        if (me < world && me != rank) {
+          const int g = pair_ctas(s_sb[me], a.gmax);
+          const Span sp = span_of(s_sb[me], slot, g, pair_chunk(s_sb[me], g), t, s);
+          if (r < sp.n) {
+            ++sent;
+            publish(&S.pad[me]->flag[par][s][rank],
+                    make_flag(epoch, pair_sig(a.sig_base, s_sb[me]), uint32_t(sent)));
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------- receiver
+  {  // local segment: straight copy (skipped when in place)
+    int64_t lo, hi;
+    byte_share(s_sb[rank], s, a.gp, lo, hi);
+    block_copy<4>(s_rp[rank] + lo, s_sp[rank] + lo, hi - lo);
+  }
   int64_t rmax = 0;
-  for (int j = 0; j < world; ++j) {
-    if (j == rank) continue;
-    if (b < s_gs[j]) rmax = max(rmax, rounds_for(s_sb[j], slot));
-    if (b < s_gr[j]) rmax = max(rmax, rounds_for(s_rb[j], slot));
-  }
-
-  // Local segment: straight copy over every launched CTA, no workspace
-  // (skipped when in place).
-  {
-    int64_t s, e;
-    byte_share(s_sb[rank], b, G, s, e);
-    block_copy<4>(s_rp[rank] + s, s_sp[rank] + s, e - s);
-  }
-
+  for (int i = 0; i < world; ++i)
+    if (i != rank && s < pair_ctas(s_rb[i], a.gmax)) rmax = max(rmax, rounds_for(s_rb[i], slot));
+  int got = 0;  // chunks consumed from peer `me`
   const uint8_t* my_ws = S.ws[rank] + hoff;
   for (int64_t t = 0; t < rmax; ++t) {
-    // Slot reuse: wait until receiver j consumed round t-1.
-    if (t > 0) {
-      if (tid < world && tid != rank && b < s_gs[tid] && t < rounds_for(s_sb[tid], slot)) {
-        int e = wait_flag(&S.pad[rank]->ack[par][b][tid], S.pad[rank], c.timeout_ns, epoch,
-                          pair_sig(a.sig_base, s_sb[tid]), uint32_t(t - 1));
-        if (e) atomicCAS(&s_err, 0, e);
+    int rows = 0;
+    for (int i = 0; i < world; ++i) {
+      if (i == rank) continue;
+      const int g = pair_ctas(s_rb[i], a.gmax);
+      rows = max(rows, span_of(s_rb[i], slot, g, pair_chunk(s_rb[i], g), t, s).n);
+    }
+    for (int r = 0; r < rows; ++r) {
+      if (me < world && me != rank) {
+        const int g = pair_ctas(s_rb[me], a.gmax);
+        const Span sp = span_of(s_rb[me], slot, g, pair_chunk(s_rb[me], g), t, s);
+        if (r < sp.n) {
+          int e = wait_flag(&S.pad[rank]->flag[par][s][me], S.pad[rank], c.timeout_ns, epoch,
+                            pair_sig(a.sig_base, s_rb[me]), uint32_t(got + 1));
+          if (e) atomicCAS(&s_err, 0, e);
+          ++got;
+        }
       }
       __syncthreads();
       if (s_err) {
         if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
         return;
       }
+      for (int k = 1; k < world; ++k) {
+        const int i = (rank - k + world) % world;
+        const int g = pair_ctas(s_rb[i], a.gmax);
+        const int64_t ch = pair_chunk(s_rb[i], g);
+        const Span sp = span_of(s_rb[i], slot, g, ch, t, s);
+        if (r >= sp.n) continue;
+        const int64_t lo = sp.a + r * ch, hi = min(sp.e, lo + ch);
+        block_copy<4>(s_rp[i] + t * slot + lo, my_ws + int64_t(i) * slot + lo, hi - lo);
+      }
     }
-    // Send round t to every peer (rotated start spreads the traffic).
-    for (int k = 1; k < world; ++k) {
-      const int j = (rank + k) % world;
-      if (b >= s_gs[j] || t >= rounds_for(s_sb[j], slot)) continue;
-      const int64_t off = t * slot;
-      const int64_t len = min(slot, s_sb[j] - off);
-      int64_t s, e;
-      byte_share(len, b, s_gs[j], s, e);
-      block_copy<4>(S.ws[j] + hoff + int64_t(rank) * slot + s, s_sp[j] + off + s, e - s);
-    }
-    __syncthreads();
-    if (tid < world && tid != rank && b < s_gs[tid] && t < rounds_for(s_sb[tid], slot))
-      publish(&S.pad[tid]->flag[par][b][rank],
-              make_flag(epoch, pair_sig(a.sig_base, s_sb[tid]), uint32_t(t)));
-    if (tid < world && tid != rank && b < s_gr[tid] && t < rounds_for(s_rb[tid], slot)) {
-      int e = wait_flag(&S.pad[rank]->flag[par][b][tid], S.pad[rank], c.timeout_ns, epoch,
-                        pair_sig(a.sig_base, s_rb[tid]), uint32_t(t));
-      if (e) atomicCAS(&s_err, 0, e);
-    }
-    __syncthreads();
-    if (s_err) {
-      if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
-      return;
-    }
-    // Receive round t from every peer into the output.
-    for (int k = 1; k < world; ++k) {
-      const int i = (rank - k + world) % world;
-      if (b >= s_gr[i] || t >= rounds_for(s_rb[i], slot)) continue;
-      const int64_t off = t * slot;
-      const int64_t len = min(slot, s_rb[i] - off);
-      int64_t s, e;
-      byte_share(len, b, s_gr[i], s, e);
-      block_copy<4>(s_rp[i] + off + s, my_ws + int64_t(i) * slot + s, e - s);
-    }
-    if (t + 1 < rmax) {
+    // Round t of every pair fully landed: let senders reuse the slot.
+    bool more = false;
+    for (int i = 0; i < world; ++i)
+      if (i != rank && s < pair_ctas(s_rb[i], a.gmax) && t + 1 < rounds_for(s_rb[i], slot)) more = true;
+    if (more) {
       __syncthreads();
-      if (tid < world && tid != rank && b < s_gr[tid] && t + 1 < rounds_for(s_rb[tid], slot))
-        publish(&S.pad[tid]->ack[par][b][rank],
-                make_flag(epoch, pair_sig(a.sig_base, s_rb[tid]), uint32_t(t)));
+      if (me < world && me != rank && s < pair_ctas(s_rb[me], a.gmax) &&
+          t + 1 < rounds_for(s_rb[me], slot))
+        publish(&S.pad[me]->ack[par][s][rank],
+                make_flag(epoch, pair_sig(a.sig_base, s_rb[me]), uint32_t(t + 1)));
     }
   }
 }
@@ -179,6 +241,7 @@ mcrdl_status_t launch_local_copy(void* dst, const void* src, int64_t nbytes, int
 
 mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t total_hint,
                                cudaStream_t stream) {
+  (void)total_hint;
   if (c->world == 1 && sp.d_counts == nullptr) {
     if (sp.sbytes[0] != sp.rbytes[0])
       return set_error(MCRDL_ERR_VALIDATION, "self segment: send %lld bytes, receive %lld bytes",
@@ -186,7 +249,7 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
     return launch_local_copy(sp.rptr[0], sp.sptr[0], sp.sbytes[0], c->num_sms, stream);
   }
   uint32_t epoch;
-  mcrdl_status_t st = begin_op(c, &epoch);
+  mcrdl_status_t st = begin_op(c, stream, &epoch);
   if (st != MCRDL_OK) return st;
   XArgs a;
   memset(&a, 0, sizeof(a));
@@ -199,225 +262,34 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   a.d_counts = sp.d_counts;
   a.in_base = sp.in_base;
   a.out_base = sp.out_base;
+  a.in_count = sp.in_count;
+  a.out_count = sp.out_count;
   a.esize = sp.esize;
   a.sig_base = sp.sig_base;
   a.slot = c->dc.half_bytes / c->world / 256 * 256;
-  a.in_count = sp.in_count;
-  a.out_count = sp.out_count;
-  a.gmax = 2 * c->num_sms < kMaxBlocks ? 2 * c->num_sms : kMaxBlocks;
-  // Grid: enough CTAs for the widest pair (pairs agree on their own CTA
-  // count, see pair_ctas); device-resident counts are unknown here -> gmax.
+  a.gmax = c->num_sms < kMaxBlocks ? c->num_sms : kMaxBlocks;  // 2 roles -> 2 CTAs/SM
+  if (a.gmax < 1) a.gmax = 1;
+  // CTAs per role: the widest pair (sender and receiver agree per pair,
+  // see pair_ctas); device-resident counts are unknown here -> gmax. The
+  // local copy also spreads over the receiver CTAs.
   int64_t g = 1;
   if (sp.d_counts != nullptr) {
     g = a.gmax;
   } else {
     for (int r = 0; r < c->world; ++r) {
+      if (r == c->rank) {
+        g = std::max<int64_t>(g, std::min<int64_t>(a.gmax, (sp.sbytes[r] + (1 << 20) - 1) >> 20));
+        continue;
+      }
       g = std::max<int64_t>(g, pair_ctas(sp.sbytes[r], a.gmax));
       g = std::max<int64_t>(g, pair_ctas(sp.rbytes[r], a.gmax));
     }
   }
-  (void)total_hint;
-  k_exchange<<<int(g), kThreads, 0, stream>>>(c->dc, a, epoch);
+  a.gp = int(g);
+  k_exchange<<<int(2 * g), kThreads, 0, stream>>>(c->dc, a, epoch);
   count_launch();
   MCRDL_CUDA_CHECK(cudaGetLastError());
   return MCRDL_OK;
 }
 
-static bool check_counts(const int64_t* counts, const int64_t* displs, int world, const char* what) {
-  for (int r = 0; r < world; ++r) {
-    if (counts[r] < 0 || displs[r] < 0) {
-      set_error(MCRDL_ERR_VALIDATION, "%s: counts and displacements must be >= 0", what);
-      return false;
-    }
-  }
-  return true;
-}
-
-static ExchangeSpec empty_spec(int esize, uint32_t sig_base) {
-  ExchangeSpec s;
-  memset(&s, 0, sizeof(s));
-  s.esize = esize;
-  s.sig_base = sig_base;
-  return s;
-}
-
 }  // namespace mcrdl
-
-using namespace mcrdl;
-
-extern "C" {
-
-mcrdl_status_t mcrdl_all_to_allv(mcrdl_comm* c, const void* in, void* out, const int64_t* scounts,
-                                 const int64_t* sdispls, const int64_t* rcounts,
-                                 const int64_t* rdispls, mcrdl_dtype_t dtype, mcrdl_algo_t algo,
-                                 uint64_t seq, void* stream) {
-  (void)algo;
-  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
-  const int es = elem_size(dtype);
-  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
-  if (!check_counts(scounts, sdispls, c->world, "scounts") ||
-      !check_counts(rcounts, rdispls, c->world, "rcounts"))
-    return MCRDL_ERR_VALIDATION;
-  if (in == out) {
-    for (int r = 0; r < c->world; ++r)
-      if (scounts[r] != rcounts[r] || sdispls[r] != rdispls[r])
-        return set_error(MCRDL_ERR_VALIDATION,
-                         "in-place all_to_allv needs identical send/recv layouts (snapshot the input)");
-  }
-  ExchangeSpec s = empty_spec(es, op_sig(kKindA2AV, dtype, 0, -1, 0, seq));
-  int64_t ts = 0, tr = 0;
-  for (int r = 0; r < c->world; ++r) {
-    s.sptr[r] = reinterpret_cast<const uint8_t*>(in) + sdispls[r] * es;
-    s.sbytes[r] = scounts[r] * es;
-    s.rptr[r] = reinterpret_cast<uint8_t*>(out) + rdispls[r] * es;
-    s.rbytes[r] = rcounts[r] * es;
-    ts += s.sbytes[r];
-    tr += s.rbytes[r];
-  }
-  return launch_exchange(c, s, ts > tr ? ts : tr, reinterpret_cast<cudaStream_t>(stream));
-}
-
-mcrdl_status_t mcrdl_all_to_allv_dev(mcrdl_comm* c, const void* in, uint64_t in_count, void* out,
-                                     uint64_t out_count, const int64_t* d_counts,
-                                     mcrdl_dtype_t dtype, mcrdl_algo_t algo,
-                                     uint64_t seq, void* stream) {
-  (void)algo;
-  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
-  const int es = elem_size(dtype);
-  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
-  if (d_counts == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL device count array");
-  ExchangeSpec s = empty_spec(es, op_sig(kKindA2AV, dtype, 0, -1, 0, seq));
-  s.d_counts = d_counts;
-  s.in_base = reinterpret_cast<const uint8_t*>(in);
-  s.out_base = reinterpret_cast<uint8_t*>(out);
-  s.in_count = int64_t(in_count);
-  s.out_count = int64_t(out_count);
-  return launch_exchange(c, s, -1, reinterpret_cast<cudaStream_t>(stream));
-}
-
-mcrdl_status_t mcrdl_all_to_all_single(mcrdl_comm* c, const void* in, void* out, uint64_t count,
-                                       mcrdl_dtype_t dtype, mcrdl_algo_t algo, uint64_t seq,
-                                       void* stream) {
-  (void)algo;
-  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
-  const int es = elem_size(dtype);
-  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
-  if (count % uint64_t(c->world) != 0)
-    return set_error(MCRDL_ERR_VALIDATION, "count %llu not divisible by %d",
-                     (unsigned long long)count, c->world);
-  const int64_t m = int64_t(count) / c->world;
-  ExchangeSpec s = empty_spec(es, op_sig(kKindA2ASingle, dtype, 0, -1, uint64_t(m), seq));
-  for (int r = 0; r < c->world; ++r) {
-    s.sptr[r] = reinterpret_cast<const uint8_t*>(in) + r * m * es;
-    s.sbytes[r] = m * es;
-    s.rptr[r] = reinterpret_cast<uint8_t*>(out) + r * m * es;
-    s.rbytes[r] = m * es;
-  }
-  return launch_exchange(c, s, int64_t(count) * es, reinterpret_cast<cudaStream_t>(stream));
-}
-
-mcrdl_status_t mcrdl_all_to_all_ptrs(mcrdl_comm* c, const void* const* in_ptrs,
-                                     const int64_t* in_counts, void* const* out_ptrs,
-                                     const int64_t* out_counts, mcrdl_dtype_t dtype,
-                                     mcrdl_algo_t algo, uint64_t seq, void* stream) {
-  (void)algo;
-  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
-  const int es = elem_size(dtype);
-  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
-  ExchangeSpec s = empty_spec(es, op_sig(kKindA2AList, dtype, 0, -1, 0, seq));
-  int64_t ts = 0, tr = 0;
-  for (int r = 0; r < c->world; ++r) {
-    if (in_counts[r] < 0 || out_counts[r] < 0)
-      return set_error(MCRDL_ERR_VALIDATION, "negative block count");
-    s.sptr[r] = reinterpret_cast<const uint8_t*>(in_ptrs[r]);
-    s.sbytes[r] = in_counts[r] * es;
-    s.rptr[r] = reinterpret_cast<uint8_t*>(out_ptrs[r]);
-    s.rbytes[r] = out_counts[r] * es;
-    ts += s.sbytes[r];
-    tr += s.rbytes[r];
-  }
-  return launch_exchange(c, s, ts > tr ? ts : tr, reinterpret_cast<cudaStream_t>(stream));
-}
-
-mcrdl_status_t mcrdl_all_gatherv(mcrdl_comm* c, const void* in, void* out, const int64_t* rcounts,
-                                 const int64_t* displs, mcrdl_dtype_t dtype, mcrdl_algo_t algo,
-                                 uint64_t seq, void* stream) {
-  (void)algo;
-  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
-  const int es = elem_size(dtype);
-  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
-  if (!check_counts(rcounts, displs, c->world, "rcounts")) return MCRDL_ERR_VALIDATION;
-  ExchangeSpec s = empty_spec(es, op_sig(kKindAllGatherv, dtype, 0, -1, 0, seq));
-  int64_t total = 0;
-  for (int r = 0; r < c->world; ++r) {
-    s.sptr[r] = reinterpret_cast<const uint8_t*>(in);
-    s.sbytes[r] = rcounts[c->rank] * es;
-    s.rptr[r] = reinterpret_cast<uint8_t*>(out) + displs[r] * es;
-    s.rbytes[r] = rcounts[r] * es;
-    total += s.rbytes[r];
-  }
-  return launch_exchange(c, s, total, reinterpret_cast<cudaStream_t>(stream));
-}
-
-mcrdl_status_t mcrdl_gatherv(mcrdl_comm* c, const void* in, void* out, const int64_t* rcounts,
-                             const int64_t* displs, int root, mcrdl_dtype_t dtype, mcrdl_algo_t algo,
-                             uint64_t seq, void* stream) {
-  (void)algo;
-  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
-  const int es = elem_size(dtype);
-  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
-  if (root < 0 || root >= c->world)
-    return set_error(MCRDL_ERR_VALIDATION, "root %d outside world %d", root, c->world);
-  if (!check_counts(rcounts, displs, c->world, "rcounts")) return MCRDL_ERR_VALIDATION;
-  if (c->rank == root && out == nullptr && rcounts[root] > 0)
-    return set_error(MCRDL_ERR_VALIDATION, "root must supply the output buffer");
-  ExchangeSpec s = empty_spec(es, op_sig(kKindGatherv, dtype, 0, root, 0, seq));
-  int64_t total = 0;
-  if (c->rank == root) {
-    for (int r = 0; r < c->world; ++r) {
-      s.rptr[r] = reinterpret_cast<uint8_t*>(out) + displs[r] * es;
-      s.rbytes[r] = rcounts[r] * es;
-      total += s.rbytes[r];
-    }
-    s.sptr[root] = reinterpret_cast<const uint8_t*>(in);
-    s.sbytes[root] = rcounts[root] * es;
-  } else {
-    s.sptr[root] = reinterpret_cast<const uint8_t*>(in);
-    s.sbytes[root] = rcounts[c->rank] * es;
-    total = s.sbytes[root];
-  }
-  return launch_exchange(c, s, total, reinterpret_cast<cudaStream_t>(stream));
-}
-
-mcrdl_status_t mcrdl_bcast(mcrdl_comm* c, void* buf, uint64_t count, mcrdl_dtype_t dtype, int root,
-                           mcrdl_algo_t algo, uint64_t seq, void* stream) {
-  (void)algo;
-  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
-  const int es = elem_size(dtype);
-  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
-  if (root < 0 || root >= c->world)
-    return set_error(MCRDL_ERR_VALIDATION, "root %d outside world %d", root, c->world);
-  if (c->world == 1) return MCRDL_OK;
-  ExchangeSpec s = empty_spec(es, op_sig(kKindBcast, dtype, 0, root, count, seq));
-  const int64_t nb = int64_t(count) * es;
-  if (c->rank == root) {
-    for (int r = 0; r < c->world; ++r) {
-      if (r == root) continue;
-      s.sptr[r] = reinterpret_cast<const uint8_t*>(buf);
-      s.sbytes[r] = nb;
-    }
-  } else {
-    s.rptr[root] = reinterpret_cast<uint8_t*>(buf);
-    s.rbytes[root] = nb;
-  }
-  return launch_exchange(c, s, nb, reinterpret_cast<cudaStream_t>(stream));
-}
-
-mcrdl_status_t mcrdl_barrier(mcrdl_comm* c, uint64_t seq, void* stream) {
-  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
-  if (c->world == 1) return MCRDL_OK;
-  ExchangeSpec s = empty_spec(1, op_sig(kKindBarrier, 0, 0, -1, 0, seq));
-  return launch_exchange(c, s, 0, reinterpret_cast<cudaStream_t>(stream));
-}
-
-}  // extern "C"

@@ -1,0 +1,207 @@
+// Public C-ABI entry points of the exchange engine (exchange.cu): each maps a
+// reference collective onto per-peer (pointer, bytes) spans.
+#include <string.h>
+
+#include "internal.h"
+
+namespace mcrdl {
+
+static bool check_counts(const int64_t* counts, const int64_t* displs, int world, const char* what) {
+  for (int r = 0; r < world; ++r) {
+    if (counts[r] < 0 || displs[r] < 0) {
+      set_error(MCRDL_ERR_VALIDATION, "%s: counts and displacements must be >= 0", what);
+      return false;
+    }
+  }
+  return true;
+}
+
+static ExchangeSpec empty_spec(int esize, uint32_t sig_base) {
+  ExchangeSpec s;
+  memset(&s, 0, sizeof(s));
+  s.esize = esize;
+  s.sig_base = sig_base;
+  return s;
+}
+
+}  // namespace mcrdl
+
+using namespace mcrdl;
+
+extern "C" {
+
+mcrdl_status_t mcrdl_all_to_allv(mcrdl_comm* c, const void* in, void* out, const int64_t* scounts,
+                                 const int64_t* sdispls, const int64_t* rcounts,
+                                 const int64_t* rdispls, mcrdl_dtype_t dtype, mcrdl_algo_t algo,
+                                 uint64_t seq, void* stream) {
+  (void)algo;
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  const int es = elem_size(dtype);
+  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+  if (!check_counts(scounts, sdispls, c->world, "scounts") ||
+      !check_counts(rcounts, rdispls, c->world, "rcounts"))
+    return MCRDL_ERR_VALIDATION;
+  // Sender and receiver CTAs run concurrently, so an aliased input could be
+  // overwritten before it is sent: the caller snapshots it (the reference
+  // does the same, collectives.py:662-663).
+  if (in == out && in != nullptr && c->world > 1)
+    return set_error(MCRDL_ERR_VALIDATION, "in-place all_to_allv: pass a snapshot of the input");
+  ExchangeSpec s = empty_spec(es, op_sig(kKindA2AV, dtype, 0, -1, 0, seq));
+  int64_t ts = 0, tr = 0;
+  for (int r = 0; r < c->world; ++r) {
+    s.sptr[r] = reinterpret_cast<const uint8_t*>(in) + sdispls[r] * es;
+    s.sbytes[r] = scounts[r] * es;
+    s.rptr[r] = reinterpret_cast<uint8_t*>(out) + rdispls[r] * es;
+    s.rbytes[r] = rcounts[r] * es;
+    ts += s.sbytes[r];
+    tr += s.rbytes[r];
+  }
+  return launch_exchange(c, s, ts > tr ? ts : tr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+mcrdl_status_t mcrdl_all_to_allv_dev(mcrdl_comm* c, const void* in, uint64_t in_count, void* out,
+                                     uint64_t out_count, const int64_t* d_counts,
+                                     mcrdl_dtype_t dtype, mcrdl_algo_t algo,
+                                     uint64_t seq, void* stream) {
+  (void)algo;
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  const int es = elem_size(dtype);
+  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+  if (d_counts == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL device count array");
+  ExchangeSpec s = empty_spec(es, op_sig(kKindA2AV, dtype, 0, -1, 0, seq));
+  s.d_counts = d_counts;
+  s.in_base = reinterpret_cast<const uint8_t*>(in);
+  s.out_base = reinterpret_cast<uint8_t*>(out);
+  s.in_count = int64_t(in_count);
+  s.out_count = int64_t(out_count);
+  return launch_exchange(c, s, -1, reinterpret_cast<cudaStream_t>(stream));
+}
+
+mcrdl_status_t mcrdl_all_to_all_single(mcrdl_comm* c, const void* in, void* out, uint64_t count,
+                                       mcrdl_dtype_t dtype, mcrdl_algo_t algo, uint64_t seq,
+                                       void* stream) {
+  (void)algo;
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  const int es = elem_size(dtype);
+  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+  if (count % uint64_t(c->world) != 0)
+    return set_error(MCRDL_ERR_VALIDATION, "count %llu not divisible by %d",
+                     (unsigned long long)count, c->world);
+  if (in == out && c->world > 1 && count > 0)
+    return set_error(MCRDL_ERR_VALIDATION, "in-place all_to_all_single: pass a snapshot of the input");
+  const int64_t m = int64_t(count) / c->world;
+  ExchangeSpec s = empty_spec(es, op_sig(kKindA2ASingle, dtype, 0, -1, uint64_t(m), seq));
+  for (int r = 0; r < c->world; ++r) {
+    s.sptr[r] = reinterpret_cast<const uint8_t*>(in) + r * m * es;
+    s.sbytes[r] = m * es;
+    s.rptr[r] = reinterpret_cast<uint8_t*>(out) + r * m * es;
+    s.rbytes[r] = m * es;
+  }
+  return launch_exchange(c, s, int64_t(count) * es, reinterpret_cast<cudaStream_t>(stream));
+}
+
+mcrdl_status_t mcrdl_all_to_all_ptrs(mcrdl_comm* c, const void* const* in_ptrs,
+                                     const int64_t* in_counts, void* const* out_ptrs,
+                                     const int64_t* out_counts, mcrdl_dtype_t dtype,
+                                     mcrdl_algo_t algo, uint64_t seq, void* stream) {
+  (void)algo;
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  const int es = elem_size(dtype);
+  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+  ExchangeSpec s = empty_spec(es, op_sig(kKindA2AList, dtype, 0, -1, 0, seq));
+  int64_t ts = 0, tr = 0;
+  for (int r = 0; r < c->world; ++r) {
+    if (in_counts[r] < 0 || out_counts[r] < 0)
+      return set_error(MCRDL_ERR_VALIDATION, "negative block count");
+    s.sptr[r] = reinterpret_cast<const uint8_t*>(in_ptrs[r]);
+    s.sbytes[r] = in_counts[r] * es;
+    s.rptr[r] = reinterpret_cast<uint8_t*>(out_ptrs[r]);
+    s.rbytes[r] = out_counts[r] * es;
+    ts += s.sbytes[r];
+    tr += s.rbytes[r];
+  }
+  return launch_exchange(c, s, ts > tr ? ts : tr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+mcrdl_status_t mcrdl_all_gatherv(mcrdl_comm* c, const void* in, void* out, const int64_t* rcounts,
+                                 const int64_t* displs, mcrdl_dtype_t dtype, mcrdl_algo_t algo,
+                                 uint64_t seq, void* stream) {
+  (void)algo;
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  const int es = elem_size(dtype);
+  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+  if (!check_counts(rcounts, displs, c->world, "rcounts")) return MCRDL_ERR_VALIDATION;
+  ExchangeSpec s = empty_spec(es, op_sig(kKindAllGatherv, dtype, 0, -1, 0, seq));
+  int64_t total = 0;
+  for (int r = 0; r < c->world; ++r) {
+    s.sptr[r] = reinterpret_cast<const uint8_t*>(in);
+    s.sbytes[r] = rcounts[c->rank] * es;
+    s.rptr[r] = reinterpret_cast<uint8_t*>(out) + displs[r] * es;
+    s.rbytes[r] = rcounts[r] * es;
+    total += s.rbytes[r];
+  }
+  return launch_exchange(c, s, total, reinterpret_cast<cudaStream_t>(stream));
+}
+
+mcrdl_status_t mcrdl_gatherv(mcrdl_comm* c, const void* in, void* out, const int64_t* rcounts,
+                             const int64_t* displs, int root, mcrdl_dtype_t dtype, mcrdl_algo_t algo,
+                             uint64_t seq, void* stream) {
+  (void)algo;
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  const int es = elem_size(dtype);
+  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+  if (root < 0 || root >= c->world)
+    return set_error(MCRDL_ERR_VALIDATION, "root %d outside world %d", root, c->world);
+  if (!check_counts(rcounts, displs, c->world, "rcounts")) return MCRDL_ERR_VALIDATION;
+  if (c->rank == root && out == nullptr && rcounts[root] > 0)
+    return set_error(MCRDL_ERR_VALIDATION, "root must supply the output buffer");
+  ExchangeSpec s = empty_spec(es, op_sig(kKindGatherv, dtype, 0, root, 0, seq));
+  int64_t total = 0;
+  if (c->rank == root) {
+    for (int r = 0; r < c->world; ++r) {
+      s.rptr[r] = reinterpret_cast<uint8_t*>(out) + displs[r] * es;
+      s.rbytes[r] = rcounts[r] * es;
+      total += s.rbytes[r];
+    }
+    s.sptr[root] = reinterpret_cast<const uint8_t*>(in);
+    s.sbytes[root] = rcounts[root] * es;
+  } else {
+    s.sptr[root] = reinterpret_cast<const uint8_t*>(in);
+    s.sbytes[root] = rcounts[c->rank] * es;
+    total = s.sbytes[root];
+  }
+  return launch_exchange(c, s, total, reinterpret_cast<cudaStream_t>(stream));
+}
+
+mcrdl_status_t mcrdl_bcast(mcrdl_comm* c, void* buf, uint64_t count, mcrdl_dtype_t dtype, int root,
+                           mcrdl_algo_t algo, uint64_t seq, void* stream) {
+  (void)algo;
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  const int es = elem_size(dtype);
+  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+  if (root < 0 || root >= c->world)
+    return set_error(MCRDL_ERR_VALIDATION, "root %d outside world %d", root, c->world);
+  if (c->world == 1) return MCRDL_OK;
+  ExchangeSpec s = empty_spec(es, op_sig(kKindBcast, dtype, 0, root, count, seq));
+  const int64_t nb = int64_t(count) * es;
+  if (c->rank == root) {
+    for (int r = 0; r < c->world; ++r) {
+      if (r == root) continue;
+      s.sptr[r] = reinterpret_cast<const uint8_t*>(buf);
+      s.sbytes[r] = nb;
+    }
+  } else {
+    s.rptr[root] = reinterpret_cast<uint8_t*>(buf);
+    s.rbytes[root] = nb;
+  }
+  return launch_exchange(c, s, nb, reinterpret_cast<cudaStream_t>(stream));
+}
+
+mcrdl_status_t mcrdl_barrier(mcrdl_comm* c, uint64_t seq, void* stream) {
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  if (c->world == 1) return MCRDL_OK;
+  ExchangeSpec s = empty_spec(1, op_sig(kKindBarrier, 0, 0, -1, 0, seq));
+  return launch_exchange(c, s, 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -52,6 +52,12 @@ struct mcrdl_comm {
   uint64_t ws_bytes = 0;
   mcrdl::DevComm dc{};
   int sticky = MCRDL_OK;              // poisoned after a device error
+  // Every op of a communicator must run in issue order on the device (flag
+  // epochs). Ops may be issued on different streams: when the stream
+  // changes, the new stream waits for the previous one (event, no host sync).
+  cudaEvent_t order_ev = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool have_last = false;
 };
 
 namespace mcrdl {
@@ -68,8 +74,9 @@ void count_launch();
                                 cudaGetErrorString(e_), __FILE__, __LINE__);          \
   } while (0)
 
-// Validates the comm and returns its next epoch (>= 1).
-mcrdl_status_t begin_op(mcrdl_comm* comm, uint32_t* epoch);
+// Validates the comm, orders `stream` after the comm's previous op and
+// returns the next epoch (>= 1).
+mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, uint32_t* epoch);
 
 inline int elem_size(mcrdl_dtype_t dt) {
   switch (dt) {

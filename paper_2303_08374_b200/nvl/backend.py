@@ -27,6 +27,7 @@ import numpy as np
 from ..collectives import ALGO_CODES, AlgorithmPolicy, canonical
 from ..core import (Buffer, CommOpKind, CommRequest, CompletionEvent, DType, HandleState,
                     WorkHandle)
+from ..dispatch import message_bytes
 from ..errors import (BackendFinalized, CommError, NativeBackendMissing, PendingAfterTimeout,
                       UnsupportedOperation, ValidationError)
 from . import _lib
@@ -126,6 +127,33 @@ class _Staging:
         self.keep.clear()
 
 
+class _Direct:
+    """Staging for the inline path: device tensors used in place on the
+    caller's stream (no record_stream, no copies)."""
+
+    __slots__ = ("device", "keep")
+
+    def __init__(self, device):
+        self.device = device
+        self.keep: list = []
+
+    def dev(self, buf: Optional[Buffer], *, upload: bool = True, download: bool = False):
+        if buf is None:
+            return None
+        t = buf.array
+        if t.device.index != self.device:
+            raise ValidationError("buffer", f"tensor on cuda:{t.device.index}, backend uses "
+                                  f"cuda:{self.device}")
+        return t
+
+    def scratch(self, count: int, dtype: DType):
+        return torch.empty(max(count, 0), dtype=dtype.torch_dtype, device=self.device)
+
+
+def _raw_stream(device: int) -> int:
+    return int(torch._C._cuda_getCurrentRawStream(device))
+
+
 def _ptr(t) -> Optional[int]:
     return None if t is None else (int(t.data_ptr()) or None)
 
@@ -152,6 +180,7 @@ class NvlBackendInstance:
         self._lock = threading.RLock()  # one host thread at a time per communicator
         self._pending: List[WorkHandle] = []
         self._errors: List[BaseException] = []
+        self._last_raw: Optional[int] = None  # stream of the most recent op
         n_dev = torch.cuda.device_count()
         dev = config.device if config.device is not None else runtime.local_device
         if dev is None:
@@ -201,6 +230,28 @@ class NvlBackendInstance:
             if t is not None:
                 name = canonical(kind, t)
         return ALGO_CODES.get(name, 0)
+
+    def inline_ok(self, request: CommRequest) -> bool:
+        """Blocking op on device tensors: run on the caller's current stream
+        with no lane hop, no events and no staging (the reference's inline
+        fast path, runtime.py:150-168). The C layer orders it after the
+        communicator's previous op even across streams."""
+        if self.runtime.log_timing:
+            return False
+        for b in request.buffers():
+            if not b.is_device:
+                return False
+        return True
+
+    def post_inline(self, request: CommRequest) -> WorkHandle:
+        if self.state != "initialized":
+            raise BackendFinalized(f"backend {self.name!r} is {self.state}")
+        with self._lock:
+            request.seq = self._seq
+            self._seq += 1
+            self._launch(request, _Direct(self.device), _raw_stream(self.device))
+            self.collectives_executed += 1
+        return WorkHandle.completed(self.name, request)
 
     def post(self, request: CommRequest) -> WorkHandle:
         if self.state != "initialized":
@@ -326,7 +377,13 @@ class NvlBackendInstance:
     def record_event(self) -> CompletionEvent:
         with self._lock:
             ev = torch.cuda.Event()
-            ev.record(self.stream)
+            # Ops of one communicator execute in issue order (the C layer
+            # chains streams), so an event after the last op covers them all.
+            last = self._last_raw
+            if last is not None and last != int(self.stream.cuda_stream):
+                ev.record(torch.cuda.ExternalStream(last, device=self.device))
+            else:
+                ev.record(self.stream)
             pending = list(self._pending)
         ce = CompletionEvent(self.name, cuda_event=ev)
         ce._pending = pending  # type: ignore[attr-defined]
@@ -335,7 +392,6 @@ class NvlBackendInstance:
     def settle(self, event: CompletionEvent) -> None:
         """After `event` fired: settle every handle it covers."""
         for h in getattr(event, "_pending", []):
-            h.test() if h.event is not None else None
             if not h.test():
                 h._settle()
         with self._lock:
@@ -356,12 +412,14 @@ class NvlBackendInstance:
     def _launch(self, req: CommRequest, st: _Staging, s: int) -> None:
         lib, c = self.comm.lib, self.comm.handle
         kind, p, rank, seq = req.kind, self.world_size, self.rank, req.seq
-        from ..dispatch import message_bytes
-
-        nbytes = message_bytes(req, p)
-        algo = self._algo_code(kind, nbytes)
-        req._algorithm = next((k for k, v in ALGO_CODES.items() if v == algo), "auto")
+        name = self.policy.algorithm(kind)
+        if name == "auto" and self.runtime.tuning_table is not None:
+            algo = self._algo_code(kind, message_bytes(req, p))
+        else:
+            algo = ALGO_CODES.get(name, 0)
+        req._algorithm = _ALGO_NAMES.get(algo, "auto")
         chk = _lib.check
+        self._last_raw = s
 
         if kind in (CommOpKind.all_reduce, CommOpKind.reduce, CommOpKind.reduce_scatter):
             i = st.dev(req.input)
@@ -449,6 +507,9 @@ class NvlBackendInstance:
             o = i if same else st.dev(req.output, upload=False, download=True)
             if same:
                 st.dev(req.output, download=True)
+            if o.numel() and i.data_ptr() == o.data_ptr() and p > 1:
+                i = i.clone()  # the reference snapshots aliased input (collectives.py:662-663)
+                st.keep.append(i)
             chk(lib.mcrdl_all_to_all_single(c, _ptr(i), _ptr(o), req.input.count,
                                             req.input.dtype.code, algo, seq, s))
             return
@@ -477,13 +538,16 @@ class NvlBackendInstance:
                                               dt.code, algo, seq, s))
                 return
             sc, sd, rc, rd = (list(map(int, v)) for v in vecs)
-            if i.data_ptr() == o.data_ptr() and (sc != rc or sd != rd):
+            if o.numel() and i.data_ptr() == o.data_ptr() and p > 1:
                 i = i.clone()  # the reference snapshots aliased input (collectives.py:662-663)
             chk(lib.mcrdl_all_to_allv(c, _ptr(i), _ptr(o), _lib.i64_array(sc), _lib.i64_array(sd),
                                       _lib.i64_array(rc), _lib.i64_array(rd), dt.code, algo, seq, s))
             return
 
         raise UnsupportedOperation(f"{kind.name} is not supported by the nvlink backend")
+
+
+_ALGO_NAMES = {v: k for k, v in ALGO_CODES.items()}
 
 
 def _is_dev(x) -> bool:

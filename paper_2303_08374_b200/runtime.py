@@ -32,7 +32,7 @@ from .errors import (BackendFinalized, CommError, DuplicateBackend, NotInitializ
 from .middleware import CommLog, CompressionConfig, FusionConfig, FusionManager
 
 DEFAULT_TIMEOUT_SECS = 30.0
-DEFAULT_WORKSPACE_BYTES = 1 << 30
+DEFAULT_WORKSPACE_BYTES = 2 << 30  # two 1 GiB halves: a 512 MiB two-shot chunk per launch
 
 ENV_RANK = "MCRDL_RANK"
 ENV_WORLD_SIZE = "MCRDL_WORLD_SIZE"
@@ -94,6 +94,10 @@ class Runtime:
         self.master_port = master_port or _env_int(ENV_MASTER_PORT, default=0) or 0
         self.default_workspace_bytes = _env_int(ENV_WORKSPACE, default=DEFAULT_WORKSPACE_BYTES)
         self.comm_log = CommLog(self.rank)
+        # Device-timed CommLog records for every op (CUDA events around each
+        # op on the lane stream). Off by default: blocking device ops then
+        # take the inline path and are not logged (MCRDL_LOG_TIMING=1 to log).
+        self.log_timing = os.environ.get("MCRDL_LOG_TIMING", "0") not in ("", "0")
         self.tuning_table: Optional[dispatch.TuningTable] = None
         self._registry: Dict[str, object] = {}
         self._registry_lock = threading.Lock()
@@ -196,13 +200,17 @@ class Runtime:
         inst = self._instance(request.backend)
         if inst.state != "initialized":
             raise BackendFinalized(f"backend {request.backend!r} is finalized")
+        cfg = inst.config
+        fused = cfg.fusion is not None and self._fusion is not None and \
+            self._fusion.eligible(cfg.fusion, request)
+        if not fused and not request.async_op and inst.inline_ok(request):
+            # Blocking device op: stream-ordered, complete when enqueued.
+            return inst.post_inline(request)
         bufs = request.unique_buffers()
         for b in bufs:
             b._checkout()
-        cfg = inst.config
         try:
-            if cfg.fusion is not None and self._fusion is not None and \
-                    self._fusion.eligible(cfg.fusion, request):
+            if fused:
                 handle = self._fusion.post(inst, cfg.fusion, request)
             else:
                 handle = inst.post(request)
