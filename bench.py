@@ -1,0 +1,480 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 MCR-DL collective hot path.
+
+Metric (BASELINE.json): collective bus GB/s at 1/2/4/8 B200. One step = one
+all_reduce (sum, fp32, out of place) of S = 256 MiB per rank through the
+public API (Runtime.post on an nvlink backend), configs[1]'s >= 64 MB point.
+
+  value  = whole-job bus bytes / time = N * busbw, busbw = 2(N-1)/N * S / t
+           (nccl-tests definition). At N = 1 there is no bus: the step is the
+           local-copy floor and its bytes are 2*S (read + write).
+  e2e    = the same metric through the same API with HOST (pinned) buffers:
+           H2D of the input, the collective, D2H of the result, per step.
+  roofline: dominant kernel (k_ar_pipe for N > 1, k_copy for N = 1),
+           algorithmic bytes per launch / mean launch time (CUDA events on
+           the launching stream) vs NVLink 900 GB/s/direction (N > 1) or
+           the measured HBM copy peak (N = 1).
+  cpu_baseline: the reference package itself (baseline/_ref, pure Python +
+           numpy, thread world of N ranks) on a bounded sample, rank 0, N=1.
+
+  --impl reference  times the reference's own CPU implementation (same
+           metric and config, bounded sample) on rank 0; other ranks exit.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+       (N > 1: launched under torch.distributed.run, one process per GPU)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MIB = 1 << 20
+METRIC = "Collective bus GB/s vs message size at 2/4/8 B200 (alltoallv, allreduce)"
+NVLINK_PEAK = 900.0  # GB/s per direction per GPU (north_star nominal)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("native", "reference"), default="native")
+    ap.add_argument("--size-mib", type=int, default=256)
+    ap.add_argument("--no-secondary", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def bus_bytes(n: int, size: int) -> float:
+    """Per-rank bus bytes of one all_reduce (p = 1: local copy read+write)."""
+    return 2.0 * size if n == 1 else 2.0 * (n - 1) / n * size
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.window = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.device), "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.monotonic(), line.strip()))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        rows = self.rows
+        if self.window:
+            inside = [r for r in rows if self.window[0] - 0.05 <= r[0] <= self.window[1] + 0.05]
+            rows = inside or rows
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for _t, line in rows:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ reference arm
+def reference_allreduce(p: int, size: int, steps: int, warmup: int):
+    """The reference's own CPU path (baseline/_ref mcrdl, public API, thread
+    world over inproc, default ring policy; tuner.py:151-214 method)."""
+    sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+    import numpy as np
+    from mcrdl import BackendConfig, Buffer, CommOpKind, CommRequest, DType, ReduceOp, run_thread_world
+
+    n = size // 4
+
+    def entry(rt, rank):
+        rt.init([BackendConfig("a", transport="inproc")])
+        rng = np.random.default_rng(rank)
+        a = Buffer(rng.standard_normal(n).astype(np.float32))
+        b = Buffer.zeros(DType.f32, n)
+        z = Buffer.zeros(DType.f32, 0)
+        out = []
+        for it in range(warmup + steps):
+            rt.post(CommRequest(CommOpKind.all_reduce, input=z, output=z, op=ReduceOp.sum,
+                                backend="a"))
+            t0 = time.perf_counter()
+            rt.post(CommRequest(CommOpKind.all_reduce, input=a, output=b, op=ReduceOp.sum,
+                                backend="a"))
+            dt = time.perf_counter() - t0
+            if it >= warmup:
+                out.append(dt)
+        d = Buffer(np.array(out, dtype=np.float64))
+        if p > 1:
+            rt.all_reduce("a", d, ReduceOp.max)
+        rt.finalize()
+        return d.array.tolist()
+
+    res = run_thread_world(p, entry, timeout=600.0, join_timeout=3600.0)
+    per_step = res[0]
+    t = statistics.median(per_step)
+    return t, per_step
+
+
+def cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count(), model
+
+
+def run_reference(args) -> int:
+    rank = int(os.environ.get("RANK", "0"))
+    n = args.gpus
+    if rank != 0:
+        return 0
+    # Bounded sample: S_ref per rank sized so the run stays within minutes.
+    size = min(args.size_mib, 32 if n <= 2 else 16) * MIB
+    steps = max(3, min(args.steps, 10))
+    warmup = max(1, min(args.warmup, 3))
+    t, _ = reference_allreduce(n, size, steps, warmup)
+    value = n * bus_bytes(n, size) / t / 1e9
+    cores, model = cpu_info()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": n, "steps": steps, "warmup": warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (standard normal)",
+        "config": {"workload": f"all_reduce sum f32, {size // MIB} MiB per rank (bounded sample "
+                               f"of the {args.size_mib} MiB config), world {n}",
+                   "op": "all_reduce", "world": n, "bytes_per_rank": size,
+                   "algorithm": "reference default (ring)", "l2": "host path"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": n, "kind": "reference",
+                         "sample": f"{steps} steps of all_reduce {size // MIB} MiB f32 x {n} "
+                                   f"thread-ranks (one Python process, GIL) on {model}"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- native arm
+def run_native(args) -> int:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2303_08374_b200 import BackendConfig, Buffer, CommOpKind, CommRequest, ReduceOp, Runtime
+    from paper_2303_08374_b200.nvl import _lib
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("gloo")  # host control plane (barrier, max over ranks)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    rt = Runtime(rank, world)
+    rt.init([BackendConfig("nvl", workspace_bytes=2 << 30)])
+    size = args.size_mib * MIB
+    n = size // 4
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    a = torch.randn(n, device=dev, generator=g)
+    b = torch.empty_like(a)
+    A, B = Buffer(a), Buffer(b)
+
+    def step():
+        rt.post(CommRequest(CommOpKind.all_reduce, input=A, output=B, op=ReduceOp.sum,
+                            backend="nvl"))
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    stream = torch.cuda.current_stream()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = _lib.launch_count()
+    t_wall0 = time.monotonic()
+    s.record(stream)
+    for _ in range(args.steps):
+        step()
+    e.record(stream)
+    e.synchronize()
+    t_wall1 = time.monotonic()
+    launches = _lib.launch_count() - l0
+    barrier()
+    clocks.mark(t_wall0, t_wall1)
+    ms = s.elapsed_time(e) / args.steps
+    ms = max_over_ranks(ms)
+    t = ms * 1e-3
+    rt.synchronize()  # surfaces any latched device error
+    value = world * bus_bytes(world, size) / t / 1e9
+    per_launch_bytes = bus_bytes(world, size) * args.steps / max(launches, 1)
+    t_launch = t * args.steps / max(launches, 1)
+    peaks = measured_peaks()
+    if world == 1:
+        peak, peak_src, bound = float(peaks.get("hbm_gbs", 6650.0)), \
+            "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6.65 TB/s", "hbm"
+    else:
+        peak, peak_src, bound = NVLINK_PEAK, "NVLink 5 nominal per direction (north_star)", "nvlink"
+    achieved = per_launch_bytes / t_launch / 1e9
+    clk = clocks.stop()
+
+    # ---- e2e: host (pinned) buffers through the same public API
+    ha = torch.randn(n, generator=torch.Generator().manual_seed(99 + rank)).pin_memory()
+    hb = torch.empty(n, dtype=torch.float32).pin_memory()
+    HA, HB = Buffer(ha), Buffer(hb)
+
+    def e2e_step():
+        rt.post(CommRequest(CommOpKind.all_reduce, input=HA, output=HB, op=ReduceOp.sum,
+                            backend="nvl"))
+
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()  # blocking: returns after the D2H copy landed in hb
+    t_e2e = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    e2e_value = world * bus_bytes(world, size) / t_e2e / 1e9
+
+    # ---- NCCL comparator + secondary workloads (N > 1)
+    extra = {}
+    if world > 1 and not args.no_secondary:
+        extra = secondary(rt, world, rank, dev, size, barrier, max_over_ranks)
+    # ---- CPU baseline (reference package, rank 0, N == 1)
+    cpu = None
+    if rank == 0 and world == 1:
+        try:
+            csz = 32 * MIB
+            tc, _ = reference_allreduce(1, csz, 10, 2)
+            cores, model = cpu_info()
+            cpu = {"value": bus_bytes(1, csz) / tc / 1e9, "unit": "GB/s", "cores": 1,
+                   "kind": "reference",
+                   "sample": f"10 steps of all_reduce f32 {csz // MIB} MiB, world 1, reference "
+                             f"mcrdl (baseline/_ref) on {model}"}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                   "sample": f"failed: {exc!r}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (torch.randn, seeded per rank)",
+            "config": {
+                "workload": f"all_reduce sum f32 out-of-place, {args.size_mib} MiB per rank, "
+                            f"world {world} (BASELINE configs[1] point >= 64 MB)",
+                "op": "all_reduce", "world": world, "bytes_per_rank": size,
+                "algorithm": "auto (library size heuristic: two_shot >= 512 KiB)",
+                "value_definition": ("N * busbw, busbw = 2(N-1)/N*S/t" if world > 1 else
+                                     "2*S/t (local-copy floor: read + write)"),
+                "busbw_gbs_per_rank": bus_bytes(world, size) / t / 1e9,
+                "frac_of_900": (bus_bytes(world, size) / t / 1e9 / NVLINK_PEAK) if world > 1 else None,
+                "l2": f"inputs {args.size_mib} MiB > 126 MB L2 (no flush needed)",
+                "parallelism": f"{world} ranks, one process per GPU",
+            },
+            "roofline": {"bound": bound, "kernel": "k_ar_pipe" if world > 1 else "k_copy",
+                         "achieved": achieved, "peak": peak, "peak_source": peak_src,
+                         "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None,
+                         "bytes_per_launch": per_launch_bytes},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": size,
+                    "d2h_bytes_per_step": size, "ms_per_step": t_e2e * 1e3,
+                    "path": "Runtime.post on numpy-style host Buffers (pinned torch CPU tensors)"},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        line.update(extra)
+        traffic = _ncu_traffic(world)
+        if traffic is not None:
+            line["roofline"]["traffic"] = traffic
+        print(json.dumps(line), flush=True)
+    rt.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _ncu_traffic(world: int):
+    """dram read+write bytes per launch of the dominant kernel from the
+    committed `ncu --set full` capture (profiles/ncu_traffic.json), if any."""
+    try:
+        doc = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        return doc.get(str(world))
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def secondary(rt, world, rank, dev, size, barrier, max_over_ranks):
+    """NCCL comparator at the headline size, DLRM all_to_allv (cfg4) and
+    DS-MoE all_to_all_single (cfg3 shape) on the same ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2303_08374_b200 import Buffer
+
+    out = {}
+    iters = 10
+
+    def dev_time(fn, reps=iters):
+        for _ in range(3):
+            fn()
+        barrier()
+        st = torch.cuda.current_stream()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(st)
+        for _ in range(reps):
+            fn()
+        e.record(st)
+        e.synchronize()
+        return max_over_ranks(s.elapsed_time(e) / reps * 1e-3)
+
+    # NCCL comparator (torch.distributed, same size and dtype)
+    try:
+        pg = dist.new_group(backend="nccl")
+        x = torch.randn(size // 4, device=dev)
+        t = dev_time(lambda: dist.all_reduce(x, group=pg))
+        out["nccl_all_reduce"] = {"busbw_gbs": bus_bytes(world, size) / t / 1e9,
+                                  "ms": t * 1e3, "bytes_per_rank": size}
+    except Exception as exc:  # noqa: BLE001
+        pg = None
+        out["nccl_all_reduce"] = {"error": repr(exc)}
+
+    # DLRM cfg4: 26 tables, dim 128, f32, global batch 65536, uniform local batch
+    tables = [len(x) for x in _array_split(26, world)]
+    B = 65536
+    b = B // world
+    sc = [b * tables[rank] * 128 for _ in range(world)]
+    rc = [b * tables[j] * 128 for j in range(world)]
+    sd = [sum(sc[:j]) for j in range(world)]
+    rdp = [sum(rc[:j]) for j in range(world)]
+    inp = torch.randn(sum(sc), device=dev)
+    outp = torch.empty(sum(rc), device=dev)
+    I, O = Buffer(inp), Buffer(outp)
+    t = dev_time(lambda: rt.all_to_allv("nvl", O, I, sc, rc, sd, rdp))
+    egress = max(sum(sc) - sc[rank], sum(rc) - rc[rank]) * 4
+    egress = max_over_ranks(egress)
+    res = {"busbw_gbs": egress / t / 1e9, "ms": t * 1e3, "max_pair_egress_bytes": egress,
+           "workload": "cfg4 DLRM 26 tables x dim 128 f32, batch 65536 (uniform)"}
+    if pg is not None:
+        try:
+            t2 = dev_time(lambda: dist.all_to_all_single(outp, inp, rc, sc, group=pg))
+            res["nccl_busbw_gbs"] = egress / t2 / 1e9
+        except Exception as exc:  # noqa: BLE001
+            res["nccl_error"] = repr(exc)
+    out["all_to_allv_dlrm"] = res
+    # DS-MoE cfg3 shape: 4096 tokens x 4096 hidden bf16 per rank, all_to_all_single
+    x = torch.randn(4096 * 4096, device=dev).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    X, Y = Buffer(x), Buffer(y)
+    t = dev_time(lambda: rt.all_to_all_single("nvl", Y, X))
+    nb = x.numel() * 2 * (world - 1) / world
+    res = {"busbw_gbs": nb / t / 1e9, "ms": t * 1e3,
+           "workload": "cfg3 DS-MoE a2a 4096x4096 bf16 per rank"}
+    if pg is not None:
+        try:
+            t2 = dev_time(lambda: dist.all_to_all_single(y, x, group=pg))
+            res["nccl_busbw_gbs"] = nb / t2 / 1e9
+        except Exception as exc:  # noqa: BLE001
+            res["nccl_error"] = repr(exc)
+    out["all_to_all_moe"] = res
+    return out
+
+
+def _array_split(n, parts):
+    q, r = divmod(n, parts)
+    out, o = [], 0
+    for i in range(parts):
+        k = q + (1 if i < r else 0)
+        out.append(list(range(o, o + k)))
+        o += k
+    return out
+
+
+def main() -> int:
+    args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not under torchrun: relaunch one process per GPU
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+               "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+               "--master-port", os.environ.get("MASTER_PORT", "29533"), __file__] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_native(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,130 @@
+"""Generate golden fixtures from the REFERENCE implementation (test infra).
+
+Run here, where /root/reference exists (the GPU box never reads it):
+
+    python oracle/make_golden.py            # writes tests/golden/*.json
+
+Fixtures:
+  selftest_p{2,4,8}.json  the reference CLI's own parity dump
+                          (`mcrdl launch -n P selftest --out`, cli.py:476-491):
+                          78 cases per world, all kinds, f32/i64, counts 0/1/5.
+  live_cases.json         seeded cases (reference tests/cases.py make_case
+                          input distributions) executed by the reference's LIVE
+                          collective algorithms (run_thread_world, naive =
+                          ascending-fold policy and the default policy), every
+                          collective kind x p in {2,3,5,8} x {f32,i64,u8} x
+                          counts {0,1,7,64}, plus f32 all_reduce sums of 1000
+                          elements at p=4. Arrays are stored as base64 raw
+                          little-endian bytes so floats are exact.
+"""
+
+from __future__ import annotations
+
+import base64
+import importlib.util
+import json
+import os
+import subprocess
+import sys
+import zlib
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+REF_SRC = Path("/root/reference/pkg/src")
+REF_TESTS = Path("/root/reference/pkg/tests")
+OUT = ROOT / "tests" / "golden"
+
+
+def enc(a) -> dict:
+    a = np.ascontiguousarray(a)
+    return {"dtype": a.dtype.str, "b64": base64.b64encode(a.tobytes()).decode()}
+
+
+def selftest_dumps() -> None:
+    env = dict(os.environ, PYTHONPATH=str(REF_SRC))
+    for p in (2, 4, 8):
+        out = OUT / f"selftest_p{p}.json"
+        subprocess.run([sys.executable, "-m", "mcrdl", "launch", "-n", str(p), "selftest",
+                        "--out", str(out)], env=env, check=True, cwd="/tmp")
+        print("wrote", out)
+
+
+def live_cases() -> None:
+    sys.path.insert(0, str(REF_SRC))
+    sys.path.insert(0, str(REF_TESTS))
+    import mcrdl
+    from mcrdl import AlgorithmPolicy, BackendConfig, CommOpKind, DType, run_thread_world
+
+    spec = importlib.util.spec_from_file_location("ref_cases", REF_TESTS / "cases.py")
+    cases = importlib.util.module_from_spec(spec)
+    sys.modules["ref_cases"] = cases
+    spec.loader.exec_module(cases)
+
+    records = []
+
+    def run(case, policy):
+        def entry(rt, rank):
+            rt.init([BackendConfig("a", transport="inproc", policy=policy)])
+            req = case.build_request(rank, "a")
+            rt.post(req)
+            res = case.result_of(rank, req)
+            rt.finalize()
+            return res
+
+        return run_thread_world(case.p, entry, timeout=60.0)
+
+    def pack_result(kind, res):
+        if res is None:
+            return None
+        if kind is CommOpKind.all_to_all:
+            return [enc(x) for x in res]
+        return enc(res)
+
+    for kind in cases.COLLECTIVE_KINDS:
+        for p in (2, 3, 5, 8):
+            for dtype in (DType.f32, DType.i64, DType.u8):
+                for count in (0, 1, 7, 64):
+                    seed = zlib.crc32(f"{kind.value}|{p}|{dtype.name}|{count}".encode()) & 0xFFFF
+                    case = cases.make_case(kind, dtype, count, p, seed=seed)
+                    policy = AlgorithmPolicy.naive()
+                    res = run(case, policy)
+                    rec = {
+                        "kind": kind.value, "p": p, "dtype": dtype.name, "count": count,
+                        "root": case.root, "op": case.op.value, "policy": "naive",
+                        "counts": case.counts, "displs": case.displs,
+                        "sc_matrix": case.sc_matrix, "sdispls": case.sdispls,
+                        "rdispls": case.rdispls,
+                        "inputs": ([[enc(b) for b in row] for row in case.inputs]
+                                   if kind is CommOpKind.all_to_all
+                                   else [enc(x) for x in case.inputs]),
+                        "outputs": [pack_result(kind, r) for r in res],
+                    }
+                    records.append(rec)
+    # float sums with reduction-order sensitivity: naive (ascending) must be
+    # bit-exact with the oracle; ring is recorded too (within tolerance only).
+    for policy_name in ("naive", "ring"):
+        for seed in range(4):
+            case = cases.make_case(CommOpKind.all_reduce, DType.f32, 1000, 4, seed=100 + seed)
+            pol = AlgorithmPolicy.naive() if policy_name == "naive" else AlgorithmPolicy(
+                {CommOpKind.all_reduce: "ring"})
+            res = run(case, pol)
+            records.append({
+                "kind": "all_reduce", "p": 4, "dtype": "f32", "count": 1000, "root": case.root,
+                "op": "sum", "policy": policy_name, "counts": None, "displs": None,
+                "sc_matrix": None, "sdispls": None, "rdispls": None,
+                "inputs": [enc(x) for x in case.inputs],
+                "outputs": [enc(r) for r in res],
+            })
+    out = OUT / "live_cases.json"
+    out.write_text(json.dumps({"generator": "oracle/make_golden.py",
+                               "reference": "mcrdl 0.1.0 (/root/reference/pkg)",
+                               "cases": records}))
+    print("wrote", out, len(records), "cases")
+
+
+if __name__ == "__main__":
+    OUT.mkdir(parents=True, exist_ok=True)
+    selftest_dumps()
+    live_cases()

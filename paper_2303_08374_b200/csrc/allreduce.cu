@@ -328,10 +328,31 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // Local copy used for world == 1 (the p = 1 floor: out[:] = in).
+// Grid-stride (interleaved across CTAs, 4 x 16 B in flight per thread): on
+// B200 this reaches ~93% of the measured copy peak where contiguous per-CTA
+// chunks reach ~85% (tools/p2p_probe.cu, local column).
 __global__ void __launch_bounds__(kThreads) k_copy(uint8_t* dst, const uint8_t* src, int64_t n) {
-  int64_t s, e;
-  byte_share(n, blockIdx.x, gridDim.x, s, e);
-  block_copy<4>(dst + s, src + s, e - s);
+  if (((uintptr_t(dst) | uintptr_t(src)) & 15) != 0) {
+    int64_t s, e;
+    byte_share(n, blockIdx.x, gridDim.x, s, e);
+    block_copy<4>(dst + s, src + s, e - s);
+    return;
+  }
+  const int64_t np = n >> 4;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < np; i += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(s4 + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) __stcs(d4 + i + u * stride, v[u]);
+  }
+  for (; i < np; i += stride) __stcs(d4 + i, __ldcs(s4 + i));
+  if (blockIdx.x == 0)
+    for (int64_t k = (np << 4) + threadIdx.x; k < n; k += blockDim.x) dst[k] = src[k];
 }
 
 // ----------------------------------------------------------------- launch
@@ -349,8 +370,9 @@ static int grid_for(int64_t packs, int num_sms, int max_blocks) {
 mcrdl_status_t launch_local_copy(void* dst, const void* src, int64_t nbytes, int num_sms,
                                  cudaStream_t stream) {
   if (nbytes <= 0 || dst == src) return MCRDL_OK;
+  // One persistent wave (one CTA per SM) measured best for large copies.
   int64_t g = (nbytes + (int64_t(kThreads) * 64) - 1) / (int64_t(kThreads) * 64);
-  if (g > 4 * num_sms) g = 4 * num_sms;
+  if (g > num_sms) g = num_sms;
   if (g < 1) g = 1;
   k_copy<<<int(g), kThreads, 0, stream>>>(reinterpret_cast<uint8_t*>(dst),
                                           reinterpret_cast<const uint8_t*>(src), nbytes);

@@ -65,15 +65,40 @@ class NvlComm:
             self.handle = c_void_p()
 
 
-class _Staging:
-    """Maps request Buffers to device tensors for one op; host buffers go
-    through pinned memory on the lane stream and are copied back at settle."""
+class _PinnedPool:
+    """Reusable pinned host staging buffers (cudaHostAlloc is milliseconds per
+    call at hundreds of MiB; allocating per op would dominate host-buffer ops)."""
 
-    def __init__(self, device, stream):
+    def __init__(self):
+        self._free: dict = {}
+        self._lock = threading.Lock()
+
+    def get(self, numel: int, dtype):
+        key = (numel, dtype)
+        with self._lock:
+            lst = self._free.get(key)
+            if lst:
+                return lst.pop()
+        return torch.empty(numel, dtype=dtype, pin_memory=True)
+
+    def put(self, t) -> None:
+        with self._lock:
+            self._free.setdefault((t.numel(), t.dtype), []).append(t)
+
+
+class _Staging:
+    """Maps request Buffers to device tensors for one op on the lane stream.
+    Host buffers: pinned torch tensors are copied directly (H2D/D2H, async);
+    numpy arrays go through pooled pinned staging and are copied back when the
+    handle settles."""
+
+    def __init__(self, device, stream, pool: _PinnedPool):
         self.device = device
         self.stream = stream
+        self.pool = pool
         self.keep: list = []
-        self.copy_back: list = []  # (Buffer, pinned host tensor)
+        self.copy_back: list = []  # (Buffer, pinned staging or None, device tensor)
+        self._staged: list = []    # pooled pinned tensors to return at finish
         self._cache = {}
 
     def dev(self, buf: Optional[Buffer], *, upload: bool = True, download: bool = False):
@@ -82,7 +107,7 @@ class _Staging:
         key = id(buf)
         if key in self._cache:
             t = self._cache[key]
-            if download and not any(b is buf for b, _ in self.copy_back):
+            if download and not any(entry[0] is buf for entry in self.copy_back):
                 self._download(buf, t)
             return t
         if buf.is_device:
@@ -95,9 +120,14 @@ class _Staging:
             host = buf.array if buf.is_tensor else torch.from_numpy(buf.array)
             t = torch.empty(host.shape[0], dtype=host.dtype, device=self.device)
             if upload and host.shape[0]:
-                pinned = host.pin_memory() if not host.is_pinned() else host
-                t.copy_(pinned, non_blocking=True)
-                self.keep.append(pinned)
+                if host.is_pinned():
+                    src = host
+                else:
+                    src = self.pool.get(host.shape[0], host.dtype)
+                    src.copy_(host)
+                    self._staged.append(src)
+                t.copy_(src, non_blocking=True)
+                self.keep.append(host)
             if download:
                 self._download(buf, t)
         self._cache[key] = t
@@ -106,25 +136,34 @@ class _Staging:
     def _download(self, buf: Buffer, t) -> None:
         if buf.is_device:
             return
-        pinned = torch.empty(t.shape[0], dtype=t.dtype, pin_memory=True)
-        self.copy_back.append((buf, pinned, t))
+        if buf.is_tensor and buf.array.is_pinned():
+            self.copy_back.append((buf, None, t))  # D2H straight into the caller's pinned tensor
+        else:
+            pinned = self.pool.get(t.shape[0], t.dtype)
+            self._staged.append(pinned)
+            self.copy_back.append((buf, pinned, t))
 
     def issue_downloads(self) -> None:
-        for _buf, pinned, t in self.copy_back:
+        for buf, pinned, t in self.copy_back:
             if t.shape[0]:
-                pinned.copy_(t, non_blocking=True)
+                (buf.array if pinned is None else pinned).copy_(t, non_blocking=True)
 
     def scratch(self, count: int, dtype: DType):
         return torch.empty(max(count, 0), dtype=dtype.torch_dtype, device=self.device)
 
     def finish(self) -> None:
         for buf, pinned, _t in self.copy_back:
+            if pinned is None:
+                continue
             if buf.is_tensor:
                 buf.array.copy_(pinned)
             else:
                 np.copyto(buf.array, pinned.numpy())
         self.copy_back.clear()
         self.keep.clear()
+        for p in self._staged:
+            self.pool.put(p)
+        self._staged.clear()
 
 
 class _Direct:
@@ -181,6 +220,7 @@ class NvlBackendInstance:
         self._pending: List[WorkHandle] = []
         self._errors: List[BaseException] = []
         self._last_raw: Optional[int] = None  # stream of the most recent op
+        self._pool = _PinnedPool()
         n_dev = torch.cuda.device_count()
         dev = config.device if config.device is not None else runtime.local_device
         if dev is None:
@@ -265,7 +305,7 @@ class NvlBackendInstance:
             caller = torch.cuda.current_stream(self.device)
             lane = self.stream
             lane.wait_stream(caller)
-            st = _Staging(self.device, lane)
+            st = _Staging(self.device, lane, self._pool)
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(lane):
@@ -293,7 +333,7 @@ class NvlBackendInstance:
             for ev in ready_events:
                 if ev is not None:
                     lane.wait_event(ev)
-            st = _Staging(self.device, lane)
+            st = _Staging(self.device, lane, self._pool)
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             with torch.cuda.device(self.device), torch.cuda.stream(lane):

@@ -369,7 +369,125 @@ def sc_order_mismatch(cx: Ctx):
         cx.failures.append(f"order_mismatch: expected OrderMismatch, got {raised!r}")
 
 
+def sc_smoke(cx: Ctx):
+    """One small invocation of each hot-path family (smoke())."""
+    p, r = cx.p, cx.r
+    for algo in ("one_shot", "two_shot"):
+        n = 70001
+        ins = [values(DType.f32, n, "smoke", algo, q) for q in range(p)]
+        t = to_dev(ins[r], DType.f32, cx.dev)
+        cx.rt._instance(cx.b).policy = AlgorithmPolicy({CommOpKind.all_reduce: algo})
+        cx.rt.all_reduce(cx.b, Buffer(t))
+        cx.check(f"smoke/all_reduce/{algo}", from_dev(t, DType.f32), seqref.fold(ins, "sum"))
+    cx.rt._instance(cx.b).policy = AlgorithmPolicy()
+    sc = counts_matrix(p, 5000, "smoke-a2av")
+    sd = [packed(row) for row in sc]
+    rd = [packed([sc[j][q] for j in range(p)]) for q in range(p)]
+    ins = [values(DType.bf16, sum(sc[q]), "smoke-a2av-in", q) for q in range(p)]
+    want = seqref.all_to_allv(ins, sc, sd, rd, out_counts=[sum(sc[j][q] for j in range(p))
+                                                            for q in range(p)])
+    rc = [sc[j][r] for j in range(p)]
+    i = to_dev(ins[r], DType.bf16, cx.dev)
+    o = torch.zeros(sum(rc), dtype=i.dtype, device=cx.dev)
+    cx.rt.all_to_allv(cx.b, Buffer(o), Buffer(i), sc[r], rc, sd[r], rd[r])
+    cx.check("smoke/all_to_allv", from_dev(o, DType.bf16), want[r])
+
+
+def sc_golden(cx: Ctx):
+    """Replay the reference's own selftest parity dump (tests/golden/
+    selftest_p{p}.json, produced by `mcrdl launch -n p selftest --out`) and
+    the live-algorithm fixtures for this world size through the nvlink
+    backend; outputs must equal the reference's recorded outputs bit-exactly."""
+    import golden_cases as gc
+
+    p, r = cx.p, cx.r
+    dev = cx.dev
+
+    def T(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+    for case in gc.load_selftest(p):
+        op, dt = case["op"], gc.NPD[case["dtype"]]
+        root, count = case["root"], case["count"]
+        want = case["expected"][r]
+        name = f"golden/p{p}/{op}/{case['dtype']}/{count}"
+        ins = gc.selftest_arrays(case, "inputs") if "inputs" in case else None
+        got = None
+        if op == "all_reduce":
+            t = T(ins[r])
+            cx.rt.all_reduce(cx.b, Buffer(t))
+            got = t
+        elif op == "reduce":
+            t = T(ins[r])
+            cx.rt.reduce(cx.b, Buffer(t), root)
+            got = t if r == root else None
+        elif op == "bcast":
+            t = T(ins[r])
+            cx.rt.bcast(cx.b, Buffer(t), root)
+            got = t
+        elif op == "all_gather":
+            o = torch.zeros(p * count, dtype=T(ins[r]).dtype, device=dev)
+            cx.rt.all_gather(cx.b, Buffer(o), Buffer(T(ins[r])))
+            got = o
+        elif op == "gather":
+            i = T(ins[r])
+            o = torch.zeros(p * count, dtype=i.dtype, device=dev) if r == root else None
+            cx.rt.gather(cx.b, Buffer(o) if o is not None else None, Buffer(i), root)
+            got = o
+        elif op == "scatter":
+            src = T(np.asarray(case["root_input"], dtype=dt))
+            o = torch.zeros(count, dtype=src.dtype, device=dev)
+            cx.rt.scatter(cx.b, Buffer(o), Buffer(src) if r == root else None, root)
+            got = o
+        elif op == "reduce_scatter":
+            i = T(ins[r])
+            o = torch.zeros(count, dtype=i.dtype, device=dev)
+            cx.rt.reduce_scatter(cx.b, Buffer(o), Buffer(i))
+            got = o
+        elif op == "all_to_all_single":
+            i = T(ins[r])
+            o = torch.zeros_like(i)
+            cx.rt.all_to_all_single(cx.b, Buffer(o), Buffer(i))
+            got = o
+        elif op == "all_to_all":
+            x = ins[r]
+            inb = [Buffer(T(x[j * count:(j + 1) * count])) for j in range(p)]
+            outb = [Buffer(torch.zeros(count, dtype=inb[0].array.dtype, device=dev))
+                    for _ in range(p)]
+            cx.rt.all_to_all(cx.b, outb, inb)
+            got = torch.cat([b.array for b in outb]) if count else torch.zeros(0, device=dev)
+        elif op in ("gatherv", "all_gatherv"):
+            rc, dp = case["rcounts"], case["displs"]
+            i = T(ins[r])
+            if op == "all_gatherv":
+                o = torch.zeros(sum(rc), dtype=i.dtype, device=dev)
+                cx.rt.all_gatherv(cx.b, Buffer(o), Buffer(i), rc, dp)
+                got = o
+            else:
+                o = torch.zeros(sum(rc), dtype=i.dtype, device=dev) if r == root else None
+                cx.rt.gatherv(cx.b, Buffer(o) if o is not None else None, Buffer(i), root, rc, dp)
+                got = o
+        elif op == "scatterv":
+            sc, dp = case["scounts"], case["displs"]
+            src = T(np.asarray(case["root_input"], dtype=dt))
+            o = torch.zeros(sc[r], dtype=src.dtype, device=dev)
+            cx.rt.scatterv(cx.b, Buffer(o), Buffer(src) if r == root else None, root, sc, dp)
+            got = o
+        elif op == "all_to_allv":
+            sc, sd, rd = case["scounts"], case["sdispls"], case["rdispls"]
+            rc = [sc[j][r] for j in range(p)]
+            i = T(ins[r])
+            o = torch.zeros(sum(rc), dtype=i.dtype, device=dev)
+            cx.rt.all_to_allv(cx.b, Buffer(o), Buffer(i), sc[r], rc, sd[r], rd[r])
+            got = o
+        if got is None:
+            continue
+        cx.check(name, got.cpu().numpy().astype(dt), np.asarray(want, dtype=dt))
+
+
 SCENARIOS = {
+    "golden": sc_golden,
+    "smoke": sc_smoke,
     "all_reduce": sc_all_reduce,
     "all_to_allv": sc_all_to_allv,
     "all_to_all": sc_all_to_all,
@@ -384,7 +502,7 @@ SCENARIOS = {
 
 def main() -> int:
     report = sys.argv[1]
-    names = sys.argv[2].split(",") if len(sys.argv) > 2 else list(SCENARIOS)
+    names = sys.argv[2].split(",") if len(sys.argv) > 2 else [s for s in SCENARIOS if s != "smoke"]
     rank = int(os.environ["RANK"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     out = {"rank": rank, "failures": [], "checked": 0}
