@@ -237,6 +237,138 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+// ----------------------------------------------------------- NVLS (switch)
+// All-reduce through the NVSwitch multicast object (sum, f32 / bf16):
+//   copiers   [0, gp)     my input, chunk r of share s of EVERY segment ->
+//                         my NVLS buffer (local HBM copy); flag to all ranks
+//   reducers  [gp, 2gp)   chunk r of MY segment: multimem.ld_reduce (the
+//                         switch sums the p replicas) -> multimem.st (the
+//                         switch writes the sum to every rank); flag2 to all
+//   gatherers [2gp, 3gp)  chunk r of segment q once rank q's flag2 arrived:
+//                         NVLS buffer -> out
+// NVLink bytes per rank ~S each way instead of 2(p-1)/p*S for two-shot.
+// The switch's summation order is unspecified: results are within the
+// float tolerance, not bit-identical to the ascending fold.
+template <typename T>
+__device__ __forceinline__ uint4 mm_ld_reduce_sum(const void* mc) {
+  uint4 r;
+  if constexpr (sizeof(T) == 4) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(mc)
+                 : "memory");
+  } else {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(mc)
+                 : "memory");
+  }
+  return r;
+}
+__device__ __forceinline__ void mm_st(void* mc, const uint4& v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_ar_nvls(DevComm c, uint8_t* uc, uint8_t* mc, const T* in, T* out, int64_t n, int64_t sp, int gp,
+              int64_t chp, uint32_t epoch, uint32_t sig) {
+  constexpr int N = Pack<T>::N;
+  __shared__ int s_err;
+  __shared__ SComm S;
+  const int par = epoch & 1, rank = c.rank, world = c.world;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int role = int(blockIdx.x) / gp, s = int(blockIdx.x) % gp;
+  const int64_t npk = (n + N - 1) / N;
+  const int64_t rb = sp * s / gp, re = sp * (s + 1) / gp;
+  if (tid == 0) s_err = 0;
+  stage_comm(c, S);
+  __syncthreads();
+
+  if (role == 0) {  // ---------------------------------------------- copier
+    int rows = 0;
+    for (int q = 0; q < world; ++q) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
+    for (int r = 0; r < rows; ++r) {
+      for (int q = 0; q < world; ++q) {
+        const int64_t len = seg_len(npk, sp, q, rb, re);
+        const int64_t lo = int64_t(r) * chp;
+        if (lo >= len) continue;
+        const int64_t g0 = int64_t(q) * sp + rb + lo;
+        push_packs<T, VEC>(in, n, g0, min(chp, len - lo), uc + g0 * 16);
+      }
+      __syncthreads();
+      if (tid < world) publish(&S.pad[tid]->flag[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
+    }
+    return;
+  }
+
+  if (role == 1) {  // --------------------------------------------- reducer
+    const int64_t len = seg_len(npk, sp, rank, rb, re);
+    const int rows = nchunks(len, chp, s);
+    for (int r = 0; r < rows; ++r) {
+      if (tid < world) {
+        int e = wait_flag(&S.pad[rank]->flag[par][s][tid], S.pad[rank], c.timeout_ns, epoch, sig,
+                          uint32_t(r + 1));
+        if (e) atomicCAS(&s_err, 0, e);
+      }
+      __syncthreads();
+      if (s_err) {
+        if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+        return;
+      }
+      const int64_t lo = int64_t(r) * chp, hi = min(len, lo + chp);
+      const int64_t base = int64_t(rank) * sp + rb;
+      int64_t i = lo + tid;
+      for (; i + 3 * nt < hi; i += 4 * nt) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = mm_ld_reduce_sum<T>(mc + (base + i + u * nt) * 16);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mm_st(mc + (base + i + u * nt) * 16, v[u]);
+      }
+      for (; i < hi; i += nt) mm_st(mc + (base + i) * 16, mm_ld_reduce_sum<T>(mc + (base + i) * 16));
+      __threadfence_system();  // multicast stores complete on every rank before the flag
+      __syncthreads();
+      if (tid < world) publish(&S.pad[tid]->flag2[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------- gatherer
+  int rows = 0;
+  for (int q = 0; q < world; ++q) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
+  for (int r = 0; r < rows; ++r) {
+    if (tid < world && r < nchunks(seg_len(npk, sp, tid, rb, re), chp, s)) {
+      int e = wait_flag(&S.pad[rank]->flag2[par][s][tid], S.pad[rank], c.timeout_ns, epoch, sig,
+                        uint32_t(r + 1));
+      if (e) atomicCAS(&s_err, 0, e);
+    }
+    __syncthreads();
+    if (s_err) {
+      if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+      return;
+    }
+    for (int q = 0; q < world; ++q) {
+      const int64_t len = seg_len(npk, sp, q, rb, re);
+      const int64_t lo = int64_t(r) * chp;
+      if (lo >= len) continue;
+      const int64_t hi = min(len, lo + chp);
+      const int64_t base = int64_t(q) * sp + rb;
+      int64_t i = lo + tid;
+      for (; i + 3 * nt < hi; i += 4 * nt) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ld16_cg(uc + (base + i + u * nt) * 16);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) store_pack<T, VEC>(out, base + i + u * nt, n, v[u]);
+      }
+      for (; i < hi; i += nt) store_pack<T, VEC>(out, base + i, n, ld16_cg(uc + (base + i) * 16));
+    }
+  }
+}
+
 // ------------------------------------------------------------- fused (K9)
 // Members laid out back to back in a virtual packed buffer (element offsets
 // d_off[m], 16-byte aligned). One-shot protocol over the packed index space:
@@ -392,13 +524,18 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
   const int64_t bytes = n * int64_t(sizeof(T));
   const int64_t oneshot_max = half / world / 256 * 256;
   if (algo == MCRDL_ALGO_AUTO) algo = (bytes <= (int64_t(512) << 10)) ? MCRDL_ALGO_ONE_SHOT : MCRDL_ALGO_TWO_SHOT;
-  if (algo == MCRDL_ALGO_NVLS) algo = MCRDL_ALGO_TWO_SHOT;  // TODO(nvls): multicast path
+  // NVLS: the switch reduces; sum of f32/bf16 only, and only when every rank
+  // built the multicast object (caps.nvls_supported). Otherwise two-shot.
+  constexpr bool kNvlsType = (sizeof(T) == 4 && T(0.5) != T(0)) || sizeof(T) == 2;
+  if (algo == MCRDL_ALGO_NVLS && !(kNvlsType && OP == MCRDL_SUM && c->nvls.ok))
+    algo = MCRDL_ALGO_TWO_SHOT;
   if (algo == MCRDL_ALGO_ONE_SHOT && bytes > oneshot_max) algo = MCRDL_ALGO_TWO_SHOT;
 
-  // Host chunking keeps every launch inside one workspace half.
+  // Host chunking keeps every launch inside one workspace (or NVLS) half.
+  const int64_t room = (algo == MCRDL_ALGO_NVLS) ? int64_t(c->nvls.bytes / 2) : half / 2;
   const int64_t chunk_elems = (algo == MCRDL_ALGO_ONE_SHOT)
                                   ? n
-                                  : ((half / 2 - int64_t(world) * 1024) / int64_t(sizeof(T))) /
+                                  : ((room - int64_t(world) * 1024) / int64_t(sizeof(T))) /
                                         (int64_t(world) * 4 * N) * (int64_t(world) * 4 * N);
   int64_t done = 0;
   int sub = 0;
@@ -429,12 +566,29 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
       int64_t chp = (share + 3999) / 4000;  // <= 4000 chunks per share (12-bit flag step)
       if (chp < 16384) chp = 16384;         // 256 KiB chunks
       const int G = int(3 * gp);
-      if (vec)
-        k_ar_pipe<T, OP, true><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, int(gp), chp,
+      bool launched = false;
+      if constexpr (kNvlsType && OP == MCRDL_SUM) {
+        if (algo == MCRDL_ALGO_NVLS) {
+          const int64_t hoff = int64_t(epoch & 1) * int64_t(c->nvls.bytes / 2);
+          uint8_t* uc = reinterpret_cast<uint8_t*>(c->nvls.uc_ptr) + hoff;
+          uint8_t* mc = reinterpret_cast<uint8_t*>(c->nvls.mc_ptr) + hoff;
+          if (vec)
+            k_ar_nvls<T, true><<<G, kThreads, 0, stream>>>(c->dc, uc, mc, ip, op, m, sp, int(gp), chp,
                                                            epoch, sig);
-      else
-        k_ar_pipe<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, int(gp), chp,
-                                                            epoch, sig);
+          else
+            k_ar_nvls<T, false><<<G, kThreads, 0, stream>>>(c->dc, uc, mc, ip, op, m, sp, int(gp),
+                                                            chp, epoch, sig);
+          launched = true;
+        }
+      }
+      if (!launched) {
+        if (vec)
+          k_ar_pipe<T, OP, true><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, int(gp),
+                                                             chp, epoch, sig);
+        else
+          k_ar_pipe<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, int(gp),
+                                                              chp, epoch, sig);
+      }
     }
     count_launch();
     MCRDL_CUDA_CHECK(cudaGetLastError());

@@ -61,6 +61,7 @@ struct Driver {
   PFN_cuMulticastBindMem mcBindMem = nullptr;
   PFN_cuMulticastUnbind mcUnbind = nullptr;
   PFN_cuMulticastGetGranularity mcGranularity = nullptr;
+  PFN_cuDeviceGetAttribute devAttr = nullptr;
   PFN_cuGetErrorString errorString = nullptr;
   bool loaded = false;
 };
@@ -97,6 +98,7 @@ static mcrdl_status_t load_driver() {
   resolve("cuMulticastBindMem", &g_drv.mcBindMem);
   resolve("cuMulticastUnbind", &g_drv.mcUnbind);
   resolve("cuMulticastGetGranularity", &g_drv.mcGranularity);
+  resolve("cuDeviceGetAttribute", &g_drv.devAttr);
   g_drv.loaded = true;
   return MCRDL_OK;
 }
@@ -326,6 +328,125 @@ static mcrdl_status_t alloc_region(mcrdl_comm* c, uint64_t bytes, Region* rg) {
   return MCRDL_OK;
 }
 
+// Rank 0 hands one fd to every peer (the multicast object handle).
+static mcrdl_status_t bcast_fd(mcrdl_comm* c, int fd, int* out_fd) {
+  const int tag = ++g_fd_tag;
+  const double tmo = double(c->timeout_ns) * 1e-9 + 30.0;
+  if (c->rank == 0) {
+    for (int r = 1; r < c->world; ++r) {
+      mcrdl_status_t st = send_fd(c->jobid, r, 0, tag, fd, tmo);
+      if (st != MCRDL_OK) return st;
+    }
+    *out_fd = fd;
+    return MCRDL_OK;
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_stash_mu);
+    auto it = g_stash.find({tag, 0});
+    if (it != g_stash.end()) {
+      *out_fd = it->second;
+      g_stash.erase(it);
+      return MCRDL_OK;
+    }
+  }
+  for (;;) {
+    FdMsg m;
+    int got = -1;
+    mcrdl_status_t st = recv_one_fd(c->listen_fd, tmo, &m, &got);
+    if (st != MCRDL_OK) return st;
+    if (m.tag == tag && m.rank == 0) {
+      *out_fd = got;
+      return MCRDL_OK;
+    }
+    std::lock_guard<std::mutex> lk(g_stash_mu);
+    g_stash[{m.tag, m.rank}] = got;
+  }
+}
+
+// Collective: build the NVLS multicast buffer. Every rank reports whether
+// its part succeeded and NVLS is enabled only if all did (so ranks never
+// disagree on the algorithm). Failure is not an error: the communicator
+// simply has no NVLS (caps.nvls_supported = 0).
+static mcrdl_status_t setup_nvls(mcrdl_comm* c, uint64_t bytes) {
+  Nvls& nv = c->nvls;
+  int ok = 1;
+  int attr = 0;
+  if (c->world < 2 || !g_drv.mcCreate || !g_drv.mcAddDevice || !g_drv.mcBindMem ||
+      !g_drv.mcGranularity || !g_drv.devAttr)
+    ok = 0;
+  if (ok && (g_drv.devAttr(&attr, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, c->device) != CUDA_SUCCESS ||
+             attr == 0))
+    ok = 0;
+  CUmulticastObjectProp mp{};
+  size_t mg = 0;
+  if (ok) {
+    mp.numDevices = unsigned(c->world);
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    mp.size = bytes;
+    if (g_drv.mcGranularity(&mg, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS) ok = 0;
+  }
+  // Agree on attempting it at all.
+  int oks[kMaxRanks];
+  mcrdl_status_t st = host_allgather(c, &ok, oks, sizeof(int));
+  if (st != MCRDL_OK) return st;
+  for (int r = 0; r < c->world; ++r) ok &= oks[r];
+  if (!ok) return MCRDL_OK;
+  size_t gran = std::max<size_t>(mg, c->gran);
+  bytes = (bytes + 2 * gran - 1) / (2 * gran) * (2 * gran);
+  mp.size = bytes;
+  nv.bytes = bytes;
+  int fd = -1, rfd = -1;
+  if (c->rank == 0) {
+    if (g_drv.mcCreate(&nv.mc_handle, &mp) != CUDA_SUCCESS ||
+        g_drv.exportHandle(&fd, nv.mc_handle, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) !=
+            CUDA_SUCCESS)
+      ok = 0;
+  }
+  if ((st = host_allgather(c, &ok, oks, sizeof(int))) != MCRDL_OK) return st;
+  if (!oks[0]) return MCRDL_OK;
+  if ((st = bcast_fd(c, fd, &rfd)) != MCRDL_OK) return st;
+  if (c->rank != 0) {
+    if (g_drv.importHandle(&nv.mc_handle, reinterpret_cast<void*>(uintptr_t(rfd)),
+                           CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) != CUDA_SUCCESS)
+      ok = 0;
+    close(rfd);
+  } else {
+    close(fd);
+  }
+  if (ok && g_drv.mcAddDevice(nv.mc_handle, c->device) != CUDA_SUCCESS) ok = 0;
+  // Every device must join before any rank binds memory.
+  if ((st = host_allgather(c, &ok, oks, sizeof(int))) != MCRDL_OK) return st;
+  for (int r = 0; r < c->world; ++r) ok &= oks[r];
+  if (ok) {
+    CUmemAllocationProp prop = alloc_prop(c->device);
+    if (g_drv.memCreate(&nv.mem_handle, bytes, &prop, 0) != CUDA_SUCCESS) ok = 0;
+    if (ok && g_drv.mcBindMem(nv.mc_handle, 0, nv.mem_handle, 0, bytes, 0) != CUDA_SUCCESS) ok = 0;
+    nv.bound = ok;
+    if (ok && map_handle(c, nv.mc_handle, bytes, &nv.mc_ptr) != MCRDL_OK) ok = 0;
+    if (ok && map_handle(c, nv.mem_handle, bytes, &nv.uc_ptr) != MCRDL_OK) ok = 0;
+  }
+  if ((st = host_allgather(c, &ok, oks, sizeof(int))) != MCRDL_OK) return st;
+  for (int r = 0; r < c->world; ++r) ok &= oks[r];
+  nv.ok = ok != 0;
+  return MCRDL_OK;
+}
+
+static void teardown_nvls(mcrdl_comm* c) {
+  Nvls& nv = c->nvls;
+  if (nv.mc_ptr) {
+    g_drv.memUnmap(nv.mc_ptr, nv.bytes);
+    g_drv.addrFree(nv.mc_ptr, nv.bytes);
+  }
+  if (nv.uc_ptr) {
+    g_drv.memUnmap(nv.uc_ptr, nv.bytes);
+    g_drv.addrFree(nv.uc_ptr, nv.bytes);
+  }
+  if (nv.bound && g_drv.mcUnbind) g_drv.mcUnbind(nv.mc_handle, c->device, 0, nv.bytes);
+  if (nv.mem_handle) g_drv.memRelease(nv.mem_handle);
+  if (nv.mc_handle) g_drv.memRelease(nv.mc_handle);
+  nv = Nvls{};
+}
+
 mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, uint32_t* epoch) {
   if (comm == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   if (comm->sticky != MCRDL_OK)
@@ -436,6 +557,11 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   MCRDL_CUDA_CHECK(cudaMemset(reinterpret_cast<void*>(c->base.ptr[rank]), 0, kPadBytes));
   MCRDL_CUDA_CHECK(cudaDeviceSynchronize());
 
+  // NVLS buffer: half the workspace size by default; MCRDL_NVLS_BYTES=0 disables.
+  uint64_t nvls_bytes = workspace_bytes / 2;
+  if (const char* e = getenv("MCRDL_NVLS_BYTES")) nvls_bytes = strtoull(e, nullptr, 10);
+  if (nvls_bytes > 0 && (st = setup_nvls(c, nvls_bytes)) != MCRDL_OK) return fail(st);
+
   MCRDL_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int),
                                  cudaHostAllocMapped | cudaHostAllocPortable));
   *c->err_host = 0;
@@ -464,6 +590,7 @@ mcrdl_status_t mcrdl_comm_destroy(mcrdl_comm* c) {
   for (auto& rg : c->symm) unmap_region(c, rg);
   c->symm.clear();
   unmap_region(c, c->base);
+  teardown_nvls(c);
   if (c->err_host) cudaFreeHost(c->err_host);
   if (c->order_ev) cudaEventDestroy(c->order_ev);
   if (c->listen_fd >= 0) close(c->listen_fd);

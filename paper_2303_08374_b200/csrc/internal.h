@@ -23,11 +23,18 @@ struct Region {
   CUdeviceptr ptr[kMaxRanks] = {};  // rank r's region mapped here
 };
 
+// NVSwitch multicast (NVLS) buffer: one physical allocation per rank bound
+// to a multicast object; uc_ptr is this rank's own (unicast) mapping, mc_ptr
+// the multicast mapping whose loads reduce across ranks in the switch
+// (multimem.ld_reduce) and whose stores land on every rank (multimem.st).
 struct Nvls {
   bool ok = false;
   CUmemGenericAllocationHandle mc_handle = 0;
-  CUdeviceptr mc_ptr = 0;  // multicast VA covering the workspace
-  uint64_t bytes = 0;
+  CUmemGenericAllocationHandle mem_handle = 0;
+  CUdeviceptr mc_ptr = 0;
+  CUdeviceptr uc_ptr = 0;
+  uint64_t bytes = 0;  // two halves (epoch parity)
+  bool bound = false;
 };
 
 }  // namespace mcrdl

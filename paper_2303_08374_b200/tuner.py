@@ -51,10 +51,10 @@ class BenchConfig:
         if self.statistic not in STATISTICS:
             raise ValidationError("statistic", f"one of {STATISTICS}")
 
-    def candidates(self, op: CommOpKind) -> List[str]:
+    def candidates(self, op: CommOpKind, nvls: bool = False) -> List[str]:
         if self.algorithms and op in self.algorithms:
             return list(self.algorithms[op])
-        return [a for a in ALGORITHMS[op] if a not in ("auto", "nvls")]
+        return [a for a in ALGORITHMS[op] if a != "auto" and (nvls or a != "nvls")]
 
 
 @dataclass
@@ -156,7 +156,7 @@ def time_op(rt, backend: str, fn, warmup: int, iters: int, *, batch: int = 1,
         if barrier:
             rt.barrier(backend)
         if batch > 1:
-            torch.cuda._sleep(SLEEP_CYCLES)
+            torch.cuda._sleep(SLEEP_CYCLES * batch // 8)  # >= 250 us of host time per op
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
         for _ in range(batch):
@@ -187,7 +187,9 @@ def bench(rt, config: BenchConfig, backend: Optional[str] = None
     try:
         for op in config.ops:
             for nbytes in config.sizes:
-                for algo in config.candidates(op):
+                nvls = bool(inst.comm.caps.nvls_supported) and config.dtype in (DType.f32,
+                                                                                 DType.bf16)
+                for algo in config.candidates(op, nvls):
                     inst.policy = AlgorithmPolicy({op: algo})
                     try:
                         fn = make_op(rt, backend, op, nbytes, config.dtype)
@@ -297,7 +299,7 @@ def nccl_times(sizes: Sequence[int], op: CommOpKind, dtype: DType, warmup: int, 
         for _ in range(iters):
             dist.barrier()
             if batch > 1:
-                torch.cuda._sleep(SLEEP_CYCLES)
+                torch.cuda._sleep(SLEEP_CYCLES * batch // 8)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record(stream)
             for _ in range(batch):

@@ -64,7 +64,7 @@ if __name__ == "__main__":
     reps = run_world(w, sc)
     bad = 0
     for rep in reps:
-        print(f"rank {rep['rank']}: exit={rep['exit']} checked={rep['checked']} "
+        print(f"rank {rep['rank']}: exit={rep['exit']} checked={rep['checked']} nvls={rep.get('nvls')} "
               f"launches={rep.get('launches')} failures={len(rep['failures'])}")
         for f in rep["failures"][:20]:
             print("   ", f)

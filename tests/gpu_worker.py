@@ -118,6 +118,32 @@ def sc_all_reduce(cx: Ctx):
                     cx.rt.post(req)
                     cx.check(f"all_reduce/{algo}/{dtype.name}/{op}/{n}", from_dev(t, dtype), want)
     cx.rt._instance(cx.b).policy = AlgorithmPolicy()
+    # NVLS (switch reduction): f32/bf16 sums within the north_star tolerance
+    # (rtol 1e-5 f32, 1e-2 bf16, atol = rtol * max(1, max|want|)).
+    inst = cx.rt._instance(cx.b)
+    cx.nvls = bool(inst.comm.caps.nvls_supported)
+    if cx.nvls:
+        inst.policy = AlgorithmPolicy({CommOpKind.all_reduce: "nvls"})
+        for dtype, rtol in ((DType.f32, 1e-5), (DType.bf16, 1e-2)):
+            for n in (1, 7, 4097, 65536 + 3, 1 << 20, (3 << 20) + 5):
+                ins = [values(dtype, n, "nvls", dtype.name, n, q) for q in range(p)]
+                t = to_dev(ins[r], dtype, cx.dev)
+                o = torch.empty_like(t)
+                cx.rt.post(CommRequest(CommOpKind.all_reduce, input=Buffer(t), output=Buffer(o),
+                                       op=ReduceOp.sum, backend=cx.b))
+                if dtype is DType.bf16:
+                    got = seqref.bf16_bits_to_f32(from_dev(o, dtype))
+                    want = seqref.bf16_bits_to_f32(seqref.fold_bf16(ins, "sum"))
+                else:
+                    got, want = from_dev(o, dtype), seqref.fold(ins, "sum")
+                cx.check(f"all_reduce/nvls/{dtype.name}/{n}", got, want, float_reduction=True,
+                         rtol=rtol)
+        # integer / non-sum requests fall back to two-shot: still bit-exact
+        ins = [values(DType.i64, 5000, "nvls-i64", q) for q in range(p)]
+        t = to_dev(ins[r], DType.i64, cx.dev)
+        cx.rt.all_reduce(cx.b, Buffer(t))
+        cx.check("all_reduce/nvls-fallback/i64", from_dev(t, DType.i64), seqref.fold(ins, "sum"))
+        inst.policy = AlgorithmPolicy()
     # out-of-place + misaligned (element offset 1 -> scalar path)
     for dtype in (DType.f32, DType.bf16):
         n = 10001
@@ -526,6 +552,7 @@ def main() -> int:
             cx.failures.append(f"synchronize: {exc!r}")
         out["failures"] = cx.failures
         out["checked"] = cx.checked
+        out["nvls"] = getattr(cx, "nvls", None)
         out["launches"] = _lib.launch_count()
     except Exception:  # noqa: BLE001
         out["failures"].append("init/run: " + traceback.format_exc()[-3000:])
