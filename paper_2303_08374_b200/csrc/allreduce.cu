@@ -513,6 +513,16 @@ mcrdl_status_t launch_local_copy(void* dst, const void* src, int64_t nbytes, int
   return MCRDL_OK;
 }
 
+// LL threshold for one-shot all_reduce (MCRDL_LL_MAX_BYTES overrides).
+static int64_t ll_max_bytes() {
+  static int64_t v = [] {
+    const char* e = getenv("MCRDL_LL_MAX_BYTES");
+    const int64_t want = e ? int64_t(strtoll(e, nullptr, 10)) : kLLMaxAllReduceBytes;
+    return want < kLLMaxPayload ? want : kLLMaxPayload;
+  }();
+  return v;
+}
+
 template <typename T, int OP>
 static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mcrdl_algo_t algo,
                                uint64_t seq, int dt, cudaStream_t stream) {
@@ -548,6 +558,13 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
     const T* ip = in + done;
     T* op = out + done;
     const int64_t npk = (m + N - 1) / N;
+    if (algo == MCRDL_ALGO_ONE_SHOT && m * int64_t(sizeof(T)) <= ll_max_bytes()) {
+      st = launch_ar_ll<T, OP>(c, ip, op, m, epoch, sig, stream);
+      if (st != MCRDL_OK) return st;
+      done += m;
+      ++sub;
+      continue;
+    }
     if (algo == MCRDL_ALGO_ONE_SHOT) {
       const int64_t slot = (npk * 16 + 255) / 256 * 256;
       const int G = grid_for(npk, c->num_sms, 64);

@@ -35,8 +35,18 @@ struct Pad {
   uint64_t ack[2][kMaxBlocks][kMaxRanks];    // slot consumed (multi-round)
   uint64_t abort_word[2][2];                 // [par] = {epoch, code}
 };
-constexpr size_t kPadBytes = size_t(1) << 20;  // workspace starts 1 MiB into the region
-static_assert(sizeof(Pad) <= kPadBytes, "pad too large");
+// Region layout: [flag pad | LL area | workspace]. The LL area is written
+// only by LL kernels (ll.cu), so a stale LL line always carries an older
+// epoch and can never be mistaken for a current one (raw bulk payloads could
+// contain any bit pattern, including a small epoch value).
+constexpr size_t kLLOffset = size_t(1) << 20;
+constexpr int64_t kLLMaxPayload = 64 << 10;                // per (sender -> receiver) slot
+constexpr int64_t kLLSlotBytes = 33 * 4096;                // >= 16 + 2 * kLLMaxPayload
+constexpr int64_t kLLParityBytes = int64_t(kMaxRanks) * kLLSlotBytes;
+constexpr size_t kPadBytes = size_t(4) << 20;              // workspace starts 4 MiB in
+static_assert(sizeof(Pad) <= kLLOffset, "pad too large");
+static_assert(16 + 2 * kLLMaxPayload <= kLLSlotBytes, "LL slot too small");
+static_assert(kLLOffset + 2 * kLLParityBytes <= kPadBytes, "LL area too large");
 
 struct DevComm {
   uint8_t* ws[kMaxRanks];  // rank r's workspace, mapped in this address space

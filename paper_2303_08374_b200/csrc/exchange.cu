@@ -12,7 +12,7 @@
 // schedule. The grid is split into two roles that run concurrently:
 //   sender CTAs   [0, Gp)    push share s of every outgoing pair into the
 //                            peer's workspace slot `rank`, one release flag
-//                            per 64 KiB chunk;
+//                            per 256 KiB chunk;
 //   receiver CTAs [Gp, 2Gp)  copy their share of the local segment, then land
 //                            each incoming chunk as soon as its flag arrives.
 // So the NVLink push, the local copy and the copy-out overlap; senders never
@@ -23,7 +23,7 @@
 #include <algorithm>
 #include <cstring>
 
-#include "internal.h"
+#include "ll.cuh"
 
 namespace mcrdl {
 
@@ -83,6 +83,64 @@ __device__ __forceinline__ Span span_of(int64_t B, int64_t slot, int g, int64_t 
   return sp;
 }
 
+// Per-peer geometry of this CTA's role, computed once by thread `peer`:
+// 64-bit divisions are ~70-instruction subroutines, and every thread of
+// every row recomputing them cost ~8 us of latency per op.
+struct PeerGeo {
+  int64_t ch[kMaxRanks];  // chunk bytes
+  int64_t R[kMaxRanks];   // rounds this CTA takes part in (0: not serving the pair)
+  int64_t a[kMaxRanks];   // current round's share [a, e)
+  int64_t e[kMaxRanks];
+  int g[kMaxRanks];
+  int n[kMaxRanks];       // chunks of the current round's share
+  int rows;
+  int more;               // some pair continues past the current round
+  int64_t rmax;
+};
+
+__device__ __forceinline__ void geo_init(PeerGeo& G, const int64_t* bytes, int world, int rank,
+                                         int s, int gmax, int64_t slot) {
+  const int tid = threadIdx.x;
+  if (tid < world) {
+    const int64_t B = bytes[tid];
+    const int g = pair_ctas(B, gmax);
+    G.g[tid] = g;
+    G.ch[tid] = pair_chunk(B, g);
+    // LL pairs (<= kLLMaxPairBytes, ll.cuh) are moved by CTA 0 of each role.
+    G.R[tid] = (tid != rank && s < g && B > kLLMaxPairBytes) ? rounds_for(B, slot) : 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int64_t m = 0;
+    for (int j = 0; j < world; ++j) m = max(m, G.R[j]);
+    G.rmax = m;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void geo_round(PeerGeo& G, const int64_t* bytes, int world, int s,
+                                          int64_t slot, int64_t t) {
+  const int tid = threadIdx.x;
+  if (tid < world) {
+    Span sp{0, 0, 0};
+    if (t < G.R[tid]) sp = span_of(bytes[tid], slot, G.g[tid], G.ch[tid], t, s);
+    G.a[tid] = sp.a;
+    G.e[tid] = sp.e;
+    G.n[tid] = sp.n;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int rows = 0, more = 0;
+    for (int j = 0; j < world; ++j) {
+      rows = max(rows, G.n[j]);
+      if (t + 1 < G.R[j]) more = 1;
+    }
+    G.rows = rows;
+    G.more = more;
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a, uint32_t epoch) {
   __shared__ const uint8_t* s_sp[kMaxRanks];
   __shared__ uint8_t* s_rp[kMaxRanks];
@@ -90,6 +148,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a, ui
   __shared__ int64_t s_rb[kMaxRanks];
   __shared__ int s_err;
   __shared__ SComm S;
+  __shared__ PeerGeo G;
   const int par = epoch & 1, rank = c.rank, world = c.world;
   const int tid = threadIdx.x;
   const bool sender = int(blockIdx.x) < a.gp;
@@ -123,23 +182,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a, ui
     return;
   }
 
-  // Per-peer state lives in thread `peer` (tid < world) and is mirrored by
-  // every thread from shared memory when computing block-uniform loop bounds.
-  const int me = tid;  // peer index handled by this thread in flag duties
+  const int me = tid;  // peer index this thread handles in flag duties (tid < world)
   if (sender) {
-    int64_t rmax = 0;
-    for (int j = 0; j < world; ++j)
-      if (j != rank && s < pair_ctas(s_sb[j], a.gmax)) rmax = max(rmax, rounds_for(s_sb[j], slot));
-    int sent = 0;  // chunks published to peer `me` (thread-local, tid < world)
-    for (int64_t t = 0; t < rmax; ++t) {
+    if (s == 0)
+      exchange_ll_send_pairs(S.pad, rank, world, par, s_sp, s_sb, a.sig_base, epoch);
+    geo_init(G, s_sb, world, rank, s, a.gmax, slot);
+    int sent = 0;  // chunks published to peer `me`
+    for (int64_t t = 0; t < G.rmax; ++t) {
       if (t > 0) {  // slot reuse: receiver share s consumed round t-1
-        if (me < world && me != rank) {
-          const int g = pair_ctas(s_sb[me], a.gmax);
-          if (s < g && t < rounds_for(s_sb[me], slot)) {
-            int e = wait_flag(&S.pad[rank]->ack[par][s][me], S.pad[rank], c.timeout_ns, epoch,
-                              pair_sig(a.sig_base, s_sb[me]), uint32_t(t));
-            if (e) atomicCAS(&s_err, 0, e);
-          }
+        if (me < world && t < G.R[me]) {
+          int e = wait_flag(&S.pad[rank]->ack[par][s][me], S.pad[rank], c.timeout_ns, epoch,
+                            pair_sig(a.sig_base, s_sb[me]), uint32_t(t));
+          if (e) atomicCAS(&s_err, 0, e);
         }
         __syncthreads();
         if (s_err) {
@@ -147,31 +201,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a, ui
           return;
         }
       }
-      int rows = 0;
-      for (int j = 0; j < world; ++j) {
-        if (j == rank) continue;
-        const int g = pair_ctas(s_sb[j], a.gmax);
-        rows = max(rows, span_of(s_sb[j], slot, g, pair_chunk(s_sb[j], g), t, s).n);
-      }
-      for (int r = 0; r < rows; ++r) {
+      geo_round(G, s_sb, world, s, slot, t);
+      for (int r = 0; r < G.rows; ++r) {
         for (int k = 1; k < world; ++k) {
           const int j = (rank + k) % world;
-          const int g = pair_ctas(s_sb[j], a.gmax);
-          const int64_t ch = pair_chunk(s_sb[j], g);
-          const Span sp = span_of(s_sb[j], slot, g, ch, t, s);
-          if (r >= sp.n) continue;
-          const int64_t lo = sp.a + r * ch, hi = min(sp.e, lo + ch);
+          if (r >= G.n[j]) continue;
+          const int64_t lo = G.a[j] + r * G.ch[j], hi = min(G.e[j], lo + G.ch[j]);
           block_copy<4>(S.ws[j] + hoff + int64_t(rank) * slot + lo, s_sp[j] + t * slot + lo, hi - lo);
         }
         __syncthreads();
-        if (me < world && me != rank) {
-          const int g = pair_ctas(s_sb[me], a.gmax);
-          const Span sp = span_of(s_sb[me], slot, g, pair_chunk(s_sb[me], g), t, s);
-          if (r < sp.n) {
-            ++sent;
-            publish(&S.pad[me]->flag[par][s][rank],
-                    make_flag(epoch, pair_sig(a.sig_base, s_sb[me]), uint32_t(sent)));
-          }
+        if (me < world && me != rank && r < G.n[me]) {
+          ++sent;
+          publish(&S.pad[me]->flag[par][s][rank],
+                  make_flag(epoch, pair_sig(a.sig_base, s_sb[me]), uint32_t(sent)));
         }
       }
     }
@@ -184,28 +226,30 @@ __global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a, ui
     byte_share(s_sb[rank], s, a.gp, lo, hi);
     block_copy<4>(s_rp[rank] + lo, s_sp[rank] + lo, hi - lo);
   }
-  int64_t rmax = 0;
-  for (int i = 0; i < world; ++i)
-    if (i != rank && s < pair_ctas(s_rb[i], a.gmax)) rmax = max(rmax, rounds_for(s_rb[i], slot));
+  if (s == 0) {
+    const int e = exchange_ll_recv_pairs(S.pad, rank, world, par, s_rp, s_rb, a.sig_base, epoch,
+                                         c.timeout_ns);
+    if (e) {  // abort now: other threads may be polling lines that will never come
+      atomicCAS(&s_err, 0, e);
+      raise_error(S.pad, world, c.err, e, epoch);
+    }
+  }
+  __syncthreads();
+  if (s_err) {
+    if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+    return;
+  }
+  geo_init(G, s_rb, world, rank, s, a.gmax, slot);
   int got = 0;  // chunks consumed from peer `me`
   const uint8_t* my_ws = S.ws[rank] + hoff;
-  for (int64_t t = 0; t < rmax; ++t) {
-    int rows = 0;
-    for (int i = 0; i < world; ++i) {
-      if (i == rank) continue;
-      const int g = pair_ctas(s_rb[i], a.gmax);
-      rows = max(rows, span_of(s_rb[i], slot, g, pair_chunk(s_rb[i], g), t, s).n);
-    }
-    for (int r = 0; r < rows; ++r) {
-      if (me < world && me != rank) {
-        const int g = pair_ctas(s_rb[me], a.gmax);
-        const Span sp = span_of(s_rb[me], slot, g, pair_chunk(s_rb[me], g), t, s);
-        if (r < sp.n) {
-          int e = wait_flag(&S.pad[rank]->flag[par][s][me], S.pad[rank], c.timeout_ns, epoch,
-                            pair_sig(a.sig_base, s_rb[me]), uint32_t(got + 1));
-          if (e) atomicCAS(&s_err, 0, e);
-          ++got;
-        }
+  for (int64_t t = 0; t < G.rmax; ++t) {
+    geo_round(G, s_rb, world, s, slot, t);
+    for (int r = 0; r < G.rows; ++r) {
+      if (me < world && me != rank && r < G.n[me]) {
+        int e = wait_flag(&S.pad[rank]->flag[par][s][me], S.pad[rank], c.timeout_ns, epoch,
+                          pair_sig(a.sig_base, s_rb[me]), uint32_t(got + 1));
+        if (e) atomicCAS(&s_err, 0, e);
+        ++got;
       }
       __syncthreads();
       if (s_err) {
@@ -214,22 +258,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a, ui
       }
       for (int k = 1; k < world; ++k) {
         const int i = (rank - k + world) % world;
-        const int g = pair_ctas(s_rb[i], a.gmax);
-        const int64_t ch = pair_chunk(s_rb[i], g);
-        const Span sp = span_of(s_rb[i], slot, g, ch, t, s);
-        if (r >= sp.n) continue;
-        const int64_t lo = sp.a + r * ch, hi = min(sp.e, lo + ch);
+        if (r >= G.n[i]) continue;
+        const int64_t lo = G.a[i] + r * G.ch[i], hi = min(G.e[i], lo + G.ch[i]);
         block_copy<4>(s_rp[i] + t * slot + lo, my_ws + int64_t(i) * slot + lo, hi - lo);
       }
     }
     // Round t of every pair fully landed: let senders reuse the slot.
-    bool more = false;
-    for (int i = 0; i < world; ++i)
-      if (i != rank && s < pair_ctas(s_rb[i], a.gmax) && t + 1 < rounds_for(s_rb[i], slot)) more = true;
-    if (more) {
+    if (G.more) {
       __syncthreads();
-      if (me < world && me != rank && s < pair_ctas(s_rb[me], a.gmax) &&
-          t + 1 < rounds_for(s_rb[me], slot))
+      if (me < world && t + 1 < G.R[me])
         publish(&S.pad[me]->ack[par][s][rank],
                 make_flag(epoch, pair_sig(a.sig_base, s_rb[me]), uint32_t(t + 1)));
     }
@@ -251,6 +288,7 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   uint32_t epoch;
   mcrdl_status_t st = begin_op(c, stream, &epoch);
   if (st != MCRDL_OK) return st;
+  if (try_exchange_ll(c, sp, epoch, stream, &st)) return st;
   XArgs a;
   memset(&a, 0, sizeof(a));
   for (int r = 0; r < c->world; ++r) {

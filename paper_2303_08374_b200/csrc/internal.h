@@ -137,4 +137,13 @@ struct ExchangeSpec {
 mcrdl_status_t launch_exchange(mcrdl_comm* comm, const ExchangeSpec& spec, int64_t total_hint,
                                cudaStream_t stream);
 
+// LL protocol (ll.cu) for small messages.
+constexpr int64_t kLLMaxPairBytes = 64 << 10;      // exchange: every pair <= this
+constexpr int64_t kLLMaxAllReduceBytes = 64 << 10; // all_reduce one-shot message <= this
+bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, uint32_t epoch, cudaStream_t stream,
+                     mcrdl_status_t* st);
+template <typename T, int OP>
+mcrdl_status_t launch_ar_ll(mcrdl_comm* c, const T* in, T* out, int64_t n, uint32_t epoch,
+                            uint32_t sig, cudaStream_t stream);
+
 }  // namespace mcrdl

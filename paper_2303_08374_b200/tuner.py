@@ -324,7 +324,12 @@ def main(argv: Optional[List[str]] = None) -> int:
     ap.add_argument("--out", default=None, help="write the tuning table here (rank 0)")
     ap.add_argument("--csv", default=None, help="write per-cell busbw CSV here (rank 0)")
     ap.add_argument("--nccl", action="store_true", help="also time torch.distributed NCCL")
+    ap.add_argument("--api", action="store_true",
+                    help="API latency: one op per sample on an idle GPU (host enqueue included)")
     args = ap.parse_args(argv)
+    if args.api:
+        global batch_for
+        batch_for = lambda nbytes: 1  # noqa: E731
     import torch
 
     from .runtime import BackendConfig, Runtime
