@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t f = make_flag(epoch, sig, 0);
   if (tid < world && tid != rank) publish(&S.pad[tid]->flag[par][b][rank], f);
   if (tid < world && tid != rank) {
-    int e = wait_flag(&S.pad[rank]->flag[par][b][tid], S.pad[rank], c.timeout_ns, epoch, sig, 0);
+    int e = wait_flag(&S.pad[rank]->flag[par][b][tid], S.pad[rank], c.timeout_ns, c.err, epoch, sig, 0);
     if (e) atomicCAS(&s_err, 0, e);
   }
   __syncthreads();
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int rows = nchunks(len, chp, s);
     for (int r = 0; r < rows; ++r) {
       if (tid < world && tid != rank) {
-        int e = wait_flag(&S.pad[rank]->flag[par][s][tid], S.pad[rank], c.timeout_ns, epoch, sig,
+        int e = wait_flag(&S.pad[rank]->flag[par][s][tid], S.pad[rank], c.timeout_ns, c.err, epoch, sig,
                           uint32_t(r + 1));
         if (e) atomicCAS(&s_err, 0, e);
       }
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (q != rank) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
   for (int r = 0; r < rows; ++r) {
     if (tid < world && tid != rank && r < nchunks(seg_len(npk, sp, tid, rb, re), chp, s)) {
-      int e = wait_flag(&S.pad[rank]->flag2[par][s][tid], S.pad[rank], c.timeout_ns, epoch, sig,
+      int e = wait_flag(&S.pad[rank]->flag2[par][s][tid], S.pad[rank], c.timeout_ns, c.err, epoch, sig,
                         uint32_t(r + 1));
       if (e) atomicCAS(&s_err, 0, e);
     }
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int rows = nchunks(len, chp, s);
     for (int r = 0; r < rows; ++r) {
       if (tid < world) {
-        int e = wait_flag(&S.pad[rank]->flag[par][s][tid], S.pad[rank], c.timeout_ns, epoch, sig,
+        int e = wait_flag(&S.pad[rank]->flag[par][s][tid], S.pad[rank], c.timeout_ns, c.err, epoch, sig,
                           uint32_t(r + 1));
         if (e) atomicCAS(&s_err, 0, e);
       }
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   for (int q = 0; q < world; ++q) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
   for (int r = 0; r < rows; ++r) {
     if (tid < world && r < nchunks(seg_len(npk, sp, tid, rb, re), chp, s)) {
-      int e = wait_flag(&S.pad[rank]->flag2[par][s][tid], S.pad[rank], c.timeout_ns, epoch, sig,
+      int e = wait_flag(&S.pad[rank]->flag2[par][s][tid], S.pad[rank], c.timeout_ns, c.err, epoch, sig,
                         uint32_t(r + 1));
       if (e) atomicCAS(&s_err, 0, e);
     }
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   if (tid < world && tid != rank) publish(&S.pad[tid]->flag[par][b][rank], make_flag(epoch, sig, 0));
   if (tid < world && tid != rank) {
-    int e = wait_flag(&S.pad[rank]->flag[par][b][tid], S.pad[rank], c.timeout_ns, epoch, sig, 0);
+    int e = wait_flag(&S.pad[rank]->flag[par][b][tid], S.pad[rank], c.timeout_ns, c.err, epoch, sig, 0);
     if (e) atomicCAS(&s_err, 0, e);
   }
   __syncthreads();
@@ -533,7 +533,13 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
   if (world == 1) return launch_local_copy(out, in, n * int64_t(sizeof(T)), c->num_sms, stream);
   const int64_t bytes = n * int64_t(sizeof(T));
   const int64_t oneshot_max = half / world / 256 * 256;
-  if (algo == MCRDL_ALGO_AUTO) algo = (bytes <= (int64_t(512) << 10)) ? MCRDL_ALGO_ONE_SHOT : MCRDL_ALGO_TWO_SHOT;
+  if (algo == MCRDL_ALGO_AUTO) {
+    // Crossovers measured by the tuner on B200 (profiles/tune_p{2,4}.csv):
+    // one-shot pushes (p-1)*S, two-shot 2(p-1)/p*S, so it wins longer at small p.
+    const int64_t thr = world == 2 ? (int64_t(8) << 20) : world <= 4 ? (int64_t(2) << 20)
+                                                                      : (int64_t(1) << 20);
+    algo = bytes <= thr ? MCRDL_ALGO_ONE_SHOT : MCRDL_ALGO_TWO_SHOT;
+  }
   // NVLS: the switch reduces; sum of f32/bf16 only, and only when every rank
   // built the multicast object (caps.nvls_supported). Otherwise two-shot.
   constexpr bool kNvlsType = (sizeof(T) == 4 && T(0.5) != T(0)) || sizeof(T) == 2;
@@ -575,13 +581,18 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
     } else {
       const int64_t sp = (npk + world - 1) / world;
       const int64_t segb = (sp * 16 + 255) / 256 * 256;
-      // CTAs per role: one per 32 KiB of segment; 3 roles x gp <= 2 CTAs/SM.
+      // CTAs per role: one per 32 KiB of segment; 3 roles x gp <= 2 CTAs/SM
+      // (MCRDL_AR_GPMAX / MCRDL_AR_CHUNK_KB override, for tuning).
       int64_t gp = (sp * 16 + (32 << 10) - 1) / (32 << 10);
-      const int64_t gmax = 2 * c->num_sms / 3 > 0 ? 2 * c->num_sms / 3 : 1;
+      static const int64_t gp_env = env_int("MCRDL_AR_GPMAX", 0);
+      static const int64_t chunk_kb = env_int("MCRDL_AR_CHUNK_KB", 256);
+      int64_t gmax = gp_env > 0 ? gp_env : 2 * c->num_sms / 3;
+      if (gmax > kMaxBlocks) gmax = kMaxBlocks;
+      if (gmax < 1) gmax = 1;
       gp = gp < 1 ? 1 : (gp > gmax ? gmax : gp);
       const int64_t share = (sp + gp - 1) / gp;
       int64_t chp = (share + 3999) / 4000;  // <= 4000 chunks per share (12-bit flag step)
-      if (chp < 16384) chp = 16384;         // 256 KiB chunks
+      if (chp < chunk_kb * 64) chp = chunk_kb * 64;  // KiB -> 16-byte packs
       const int G = int(3 * gp);
       bool launched = false;
       if constexpr (kNvlsType && OP == MCRDL_SUM) {

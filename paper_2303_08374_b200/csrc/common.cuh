@@ -34,6 +34,7 @@ struct Pad {
   uint64_t flag2[2][kMaxBlocks][kMaxRanks];  // data-ready, phase 2
   uint64_t ack[2][kMaxBlocks][kMaxRanks];    // slot consumed (multi-round)
   uint64_t abort_word[2][2];                 // [par] = {epoch, code}
+  uint64_t poison;                           // any rank's error code, never cleared
 };
 // Region layout: [flag pad | LL area | workspace]. The LL area is written
 // only by LL kernels (ll.cu), so a stale LL line always carries an older
@@ -128,14 +129,25 @@ static __device__ __noinline__ void raise_error(Pad* const* pads, int world, int
     st_relaxed_sys(&pads[r]->abort_word[par][1], uint64_t(code));
     __threadfence_system();
     st_release_sys(&pads[r]->abort_word[par][0], uint64_t(epoch));
+    // Poison every rank: ops already enqueued behind this one (other epochs)
+    // then drain at once instead of each waiting out its timeout.
+    st_release_sys(&pads[r]->poison, uint64_t(code));
   }
 }
 
 // Spin until the flag at `p` carries (epoch, sig, >= step). Returns MCRDL_OK
 // or an error code; never spins past the timeout or a peer abort (`me` is
 // the local pad).
+// A communicator whose host-mapped error word is set is poisoned: ops that
+// were already enqueued behind the failing one must drain at once instead
+// of each waiting out its own timeout (their epochs never see the abort).
+__device__ __forceinline__ int poisoned(const int* err) {
+  return *reinterpret_cast<const volatile int*>(err);
+}
+
 static __device__ __noinline__ int wait_flag(const uint64_t* p, const Pad* me, uint64_t timeout_ns,
-                                             uint32_t epoch, uint32_t sig, uint32_t step) {
+                                             const int* err, uint32_t epoch, uint32_t sig,
+                                             uint32_t step) {
   const int par = epoch & 1;
   uint64_t start = 0;
   int spins = 0;
@@ -152,6 +164,11 @@ static __device__ __noinline__ int wait_flag(const uint64_t* p, const Pad* me, u
         int code = int(ld_relaxed_sys(&me->abort_word[par][1]));
         return code ? code : MCRDL_ERR_INTERNAL;
       }
+      // (the host-mapped `err` word is NOT polled here: a PCIe read in every
+      // spinning thread measurably slowed the bandwidth kernels; raise_error
+      // mirrors the code into every rank's device-side pad->poison instead)
+      (void)err;
+      if (const uint64_t pz = ld_relaxed_sys(&me->poison)) return int(pz);
       const uint64_t now = globaltimer_ns();
       if (start == 0) {
         start = now;

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a, ui
     for (int64_t t = 0; t < G.rmax; ++t) {
       if (t > 0) {  // slot reuse: receiver share s consumed round t-1
         if (me < world && t < G.R[me]) {
-          int e = wait_flag(&S.pad[rank]->ack[par][s][me], S.pad[rank], c.timeout_ns, epoch,
+          int e = wait_flag(&S.pad[rank]->ack[par][s][me], S.pad[rank], c.timeout_ns, c.err, epoch,
                             pair_sig(a.sig_base, s_sb[me]), uint32_t(t));
           if (e) atomicCAS(&s_err, 0, e);
         }
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a, ui
     geo_round(G, s_rb, world, s, slot, t);
     for (int r = 0; r < G.rows; ++r) {
       if (me < world && me != rank && r < G.n[me]) {
-        int e = wait_flag(&S.pad[rank]->flag[par][s][me], S.pad[rank], c.timeout_ns, epoch,
+        int e = wait_flag(&S.pad[rank]->flag[par][s][me], S.pad[rank], c.timeout_ns, c.err, epoch,
                           pair_sig(a.sig_base, s_rb[me]), uint32_t(got + 1));
         if (e) atomicCAS(&s_err, 0, e);
         ++got;

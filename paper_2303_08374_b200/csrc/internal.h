@@ -85,6 +85,11 @@ void count_launch();
 // returns the next epoch (>= 1).
 mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, uint32_t* epoch);
 
+inline int64_t env_int(const char* name, int64_t dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? int64_t(strtoll(e, nullptr, 10)) : dflt;
+}
+
 inline int elem_size(mcrdl_dtype_t dt) {
   switch (dt) {
     case MCRDL_F32: return 4;

@@ -53,6 +53,10 @@ static __device__ __noinline__ bool poll_ll(const void* p, uint32_t epoch, const
         if (*err == 0) *err = MCRDL_ERR_INTERNAL;
         return false;
       }
+      if (const uint64_t pz = ld_relaxed_sys(&me->poison)) {  // an earlier op failed
+        *err = int(pz);
+        return false;
+      }
       const uint64_t now = globaltimer_ns();
       if (start == 0) start = now;
       else if (now - start > timeout_ns) {

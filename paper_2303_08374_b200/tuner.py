@@ -190,6 +190,8 @@ def bench(rt, config: BenchConfig, backend: Optional[str] = None
                 nvls = bool(inst.comm.caps.nvls_supported) and config.dtype in (DType.f32,
                                                                                  DType.bf16)
                 for algo in config.candidates(op, nvls):
+                    if algo == "one_shot" and nbytes > inst.comm.caps.max_oneshot_bytes:
+                        continue  # the library would run two_shot: not a distinct cell
                     inst.policy = AlgorithmPolicy({op: algo})
                     try:
                         fn = make_op(rt, backend, op, nbytes, config.dtype)
@@ -324,6 +326,8 @@ def main(argv: Optional[List[str]] = None) -> int:
     ap.add_argument("--out", default=None, help="write the tuning table here (rank 0)")
     ap.add_argument("--csv", default=None, help="write per-cell busbw CSV here (rank 0)")
     ap.add_argument("--nccl", action="store_true", help="also time torch.distributed NCCL")
+    ap.add_argument("--algorithms", default=None,
+                    help="comma list restricting the candidates (e.g. two_shot,nvls)")
     ap.add_argument("--api", action="store_true",
                     help="API latency: one op per sample on an idle GPU (host enqueue included)")
     args = ap.parse_args(argv)
@@ -340,6 +344,10 @@ def main(argv: Optional[List[str]] = None) -> int:
     cfg = BenchConfig(ops=args.ops.split(","), sizes=parse_sizes(args.sizes),
                       dtype=DType.from_name(args.dtype), warmup_iters=args.warmup,
                       measure_iters=args.iters, statistic=args.statistic)
+    if args.algorithms:
+        wanted = args.algorithms.split(",")
+        cfg.algorithms = {op: [a for a in ALGORITHMS[op] if a in wanted] or ["auto"]
+                          for op in cfg.ops}
     samples, skipped = bench(rt, cfg)
     nccl = {}
     if args.nccl and rt.world_size > 1:
