@@ -103,16 +103,157 @@ __device__ __forceinline__ int nchunks(int64_t len, int64_t chp, int s) {
   return (k == 0 && s == 0) ? 1 : k;  // share 0 always carries a flag (order check)
 }
 
-template <typename T, int OP, bool VEC>
+// TMA bulk-copy streaming (one elected thread): contiguous global -> smem ring
+// (cp.async.bulk + mbarrier) -> global, possibly a peer over NVLink
+// (cp.async.bulk.global.shared::cta). Measured on B200: 16 single-thread CTAs
+// saturate NVLink push (697 GB/s, tools/tma_probe.cu) where LD/ST push needs
+// ~74 full CTAs, so the SMs stay free for the fold/gather roles.
+constexpr int kTmaStages = 4;
+constexpr int kTmaPiece = 8192;
+struct TmaRing {
+  uint8_t* buf;    // smem, kTmaStages * kTmaPiece
+  uint64_t* bar;   // smem mbarriers [kTmaStages]
+  uint32_t phase;  // parity bit per stage
+  uint32_t n;      // pieces issued
+};
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tma_init(TmaRing& R) {
+  for (int s = 0; s < kTmaStages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&R.bar[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  R.phase = 0;
+  R.n = 0;
+}
+__device__ __forceinline__ void tma_stream(TmaRing& R, uint8_t* dst, const uint8_t* src,
+                                           int64_t bytes) {
+  for (int64_t off = 0; off < bytes; off += kTmaPiece) {
+    const uint32_t sz = uint32_t(min(int64_t(kTmaPiece), bytes - off));
+    const int st = int(R.n % kTmaStages);
+    // the store issued from this stage kTmaStages pieces ago must have read smem
+    if (R.n >= kTmaStages)
+      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaStages - 1) : "memory");
+    uint8_t* buf = R.buf + st * kTmaPiece;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&R.bar[st])),
+                 "r"(sz)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(buf)),
+        "l"(src + off), "r"(sz), "r"(smem_u32(&R.bar[st]))
+        : "memory");
+    const uint32_t ph = (R.phase >> st) & 1u;
+    uint32_t ok = 0;
+    while (!ok) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(ok)
+          : "r"(smem_u32(&R.bar[st])), "r"(ph)
+          : "memory");
+    }
+    R.phase ^= (1u << st);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + off),
+                 "r"(smem_u32(buf)), "r"(sz)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    ++R.n;
+  }
+}
+// A list of contiguous copies (one row: a chunk for every peer) streamed as
+// kTmaPiece pieces with up to kTmaStages loads in flight: piece k loads into
+// stage k % kTmaStages once the store that last used that stage has read it.
+struct TmaList {
+  uint8_t* dst[kMaxRanks];
+  const uint8_t* src[kMaxRanks];
+  int64_t bytes[kMaxRanks];
+  int n;
+};
+__device__ __forceinline__ void tma_wait_stage(TmaRing& R, int st) {
+  const uint32_t ph = (R.phase >> st) & 1u;
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(&R.bar[st])), "r"(ph)
+        : "memory");
+  }
+  R.phase ^= (1u << st);
+}
+__device__ __forceinline__ void tma_copy_list(TmaRing& R, const TmaList& L) {
+  uint8_t* qdst[kTmaStages];
+  uint32_t qsz[kTmaStages];
+  int si = 0;
+  int64_t off = 0;
+  int loaded = 0, stored = 0;  // pieces of this list
+  auto next = [&](uint8_t*& d, const uint8_t*& s, uint32_t& sz) -> bool {
+    while (si < L.n && off >= L.bytes[si]) {
+      ++si;
+      off = 0;
+    }
+    if (si >= L.n) return false;
+    d = L.dst[si] + off;
+    s = L.src[si] + off;
+    sz = uint32_t(min(int64_t(kTmaPiece), L.bytes[si] - off));
+    off += sz;
+    return true;
+  };
+  auto issue_load = [&](uint8_t* d, const uint8_t* s, uint32_t sz) {
+    const int st = int((R.n + loaded) % kTmaStages);
+    if (R.n + loaded >= kTmaStages)  // stage reused: its last store must have read smem
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&R.bar[st])),
+                 "r"(sz)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(R.buf + st * kTmaPiece)),
+        "l"(s), "r"(sz), "r"(smem_u32(&R.bar[st]))
+        : "memory");
+    qdst[st] = d;
+    qsz[st] = sz;
+    ++loaded;
+  };
+  uint8_t* d;
+  const uint8_t* s;
+  uint32_t sz;
+  while (loaded < kTmaStages - 1 && next(d, s, sz)) issue_load(d, s, sz);
+  while (stored < loaded) {
+    const int st = int((R.n + stored) % kTmaStages);
+    tma_wait_stage(R, st);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(qdst[st]),
+                 "r"(smem_u32(R.buf + st * kTmaPiece)), "r"(qsz[st])
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    ++stored;
+    if (next(d, s, sz)) issue_load(d, s, sz);
+  }
+  R.n += loaded;
+}
+
+// All bulk stores issued so far are complete and ordered before the thread's
+// following generic-proxy operations (the release flag).
+__device__ __forceinline__ void tma_drain() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <typename T, int OP, bool VEC, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2)
-    k_ar_pipe(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp,
+    k_ar_pipe(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp, int gs,
               int64_t chp, uint32_t epoch, uint32_t sig) {
   constexpr int N = Pack<T>::N;
   __shared__ int s_err;
   __shared__ SComm S;
+  __shared__ __align__(128) uint8_t s_ring[TMA ? kTmaStages * kTmaPiece : 16];
+  __shared__ __align__(8) uint64_t s_bar[kTmaStages];
   const int par = epoch & 1, rank = c.rank, world = c.world;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int role = int(blockIdx.x) / gp, s = int(blockIdx.x) % gp;
+  // CTA roles: [0, gs) senders, [gs, gs+gp) reducers, [gs+gp, gs+2gp) gatherers
+  const int bid = int(blockIdx.x);
+  const int role = bid < gs ? 0 : (bid < gs + gp ? 1 : 2);
+  const int s = role == 0 ? bid : (role == 1 ? bid - gs : bid - gs - gp);
   const int64_t npk = (n + N - 1) / N;
   const int64_t rb = sp * s / gp, re = sp * (s + 1) / gp;
   const int64_t hoff = int64_t(par) * c.half_bytes;
@@ -121,6 +262,47 @@ __global__ void __launch_bounds__(kThreads, 2)
   stage_comm(c, S);
   __syncthreads();
   const uint8_t* ws = S.ws[rank] + hoff;
+
+  if (TMA && role == 0) {  // ---------------------------- sender (TMA bulk)
+    if (tid != 0) return;
+    TmaRing R{s_ring, s_bar, 0, 0};
+    tma_init(R);
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(in);
+    for (int sh = s; sh < gp; sh += gs) {  // shares served by this CTA
+      const int64_t b0 = sp * sh / gp, b1 = sp * (sh + 1) / gp;
+      int rows = 0;
+      for (int q = 0; q < world; ++q)
+        if (q != rank) rows = max(rows, nchunks(seg_len(npk, sp, q, b0, b1), chp, sh));
+      for (int r = 0; r < rows; ++r) {
+        TmaList L;
+        L.n = 0;
+        for (int k = 1; k < world; ++k) {
+          const int q = (rank + k) % world;
+          const int64_t len = seg_len(npk, sp, q, b0, b1);
+          const int64_t lo = int64_t(r) * chp;
+          if (lo >= len) continue;
+          const int64_t cnt = min(chp, len - lo);
+          const int64_t g0 = int64_t(q) * sp + b0 + lo;
+          // full packs by TMA, a trailing partial pack (end of the message) by hand
+          const int64_t full = min(cnt, n / N - g0 > 0 ? n / N - g0 : int64_t(0));
+          uint8_t* dst = S.ws[q] + hoff + int64_t(rank) * segb + (b0 + lo) * 16;
+          if (full > 0) {
+            L.dst[L.n] = dst;
+            L.src[L.n] = src + g0 * 16;
+            L.bytes[L.n] = full * 16;
+            ++L.n;
+          }
+          for (int64_t i = full; i < cnt; ++i) st16(dst + i * 16, load_pack<T, VEC>(in, g0 + i, n));
+        }
+        tma_copy_list(R, L);
+        tma_drain();
+        for (int q = 0; q < world; ++q)
+          if (q != rank && r < nchunks(seg_len(npk, sp, q, b0, b1), chp, sh))
+            publish(&S.pad[q]->flag[par][sh][rank], make_flag(epoch, sig, uint32_t(r + 1)));
+      }
+    }
+    return;
+  }
 
   if (role == 0) {  // ---------------------------------------------- sender
     int rows = 0;
@@ -610,12 +792,32 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
         }
       }
       if (!launched) {
-        if (vec)
-          k_ar_pipe<T, OP, true><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, int(gp),
-                                                             chp, epoch, sig);
-        else
-          k_ar_pipe<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, int(gp),
-                                                              chp, epoch, sig);
+        // RS senders on TMA bulk copies for large launches (aligned buffers):
+        // measured +2-3% at >= 256 MiB, slower below 64 MiB (profiles/tma_ab_r1.log).
+        // MCRDL_AR_TMA=0 disables, =2 forces; MCRDL_AR_TMA_CTAS sets the sender CTAs.
+        static const int64_t tma_on = env_int("MCRDL_AR_TMA", 1);
+        static const int64_t tma_ctas = env_int("MCRDL_AR_TMA_CTAS", 64);
+        const bool big = m * int64_t(sizeof(T)) >= (int64_t(256) << 20);
+        if (vec && (tma_on == 2 || (tma_on == 1 && big))) {
+          const int gs = int(std::min<int64_t>(gp, tma_ctas));
+          int64_t gpt = gp;
+          const int64_t cap = (2 * c->num_sms - gs) / 2;  // gs + 2*gp <= 2 CTAs/SM
+          if (gp_env <= 0 && gpt < cap) {
+            gpt = std::min<int64_t>(cap, (sp * 16 + (32 << 10) - 1) / (32 << 10));
+            if (gpt < 1) gpt = 1;
+          }
+          const int64_t sharet = (sp + gpt - 1) / gpt;
+          int64_t chpt = (sharet + 3999) / 4000;
+          if (chpt < chunk_kb * 64) chpt = chunk_kb * 64;
+          k_ar_pipe<T, OP, true, true><<<int(gs + 2 * gpt), kThreads, 0, stream>>>(
+              c->dc, ip, op, m, sp, segb, int(gpt), gs, chpt, epoch, sig);
+        } else if (vec) {
+          k_ar_pipe<T, OP, true, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb,
+                                                                    int(gp), int(gp), chp, epoch, sig);
+        } else {
+          k_ar_pipe<T, OP, false, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb,
+                                                                     int(gp), int(gp), chp, epoch, sig);
+        }
       }
     }
     count_launch();
