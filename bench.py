@@ -256,6 +256,10 @@ def run_native(args) -> int:
         rt.post(CommRequest(CommOpKind.all_reduce, input=A, output=B, op=ReduceOp.sum,
                             backend="nvl"))
 
+    # configs[1]: "algorithm chosen by tuning table" -> build it in situ for the
+    # headline cell (every candidate algorithm timed on this box and world size,
+    # cross-rank max), then the timed steps route through it.
+    tuning = autotune(rt, size, world)
     for _ in range(args.warmup):
         step()
     barrier()
@@ -336,7 +340,8 @@ def run_native(args) -> int:
                 "workload": f"all_reduce sum f32 out-of-place, {args.size_mib} MiB per rank, "
                             f"world {world} (BASELINE configs[1] point >= 64 MB)",
                 "op": "all_reduce", "world": world, "bytes_per_rank": size,
-                "algorithm": "auto (library size heuristic: two_shot >= 512 KiB)",
+                "algorithm": tuning.get("winner"),
+                "tuning_table_cell": tuning,
                 "value_definition": ("N * busbw, busbw = 2(N-1)/N*S/t" if world > 1 else
                                      "2*S/t (local-copy floor: read + write)"),
                 "busbw_gbs_per_rank": bus_bytes(world, size) / t / 1e9,
@@ -344,7 +349,9 @@ def run_native(args) -> int:
                 "l2": f"inputs {args.size_mib} MiB > 126 MB L2 (no flush needed)",
                 "parallelism": f"{world} ranks, one process per GPU",
             },
-            "roofline": {"bound": bound, "kernel": "k_ar_pipe" if world > 1 else "k_copy",
+            "roofline": {"bound": bound,
+                         "kernel": ({"nvls": "k_ar_nvls", "one_shot": "k_ar_oneshot"}.get(
+                             tuning.get("winner"), "k_ar_pipe") if world > 1 else "k_copy"),
                          "achieved": achieved, "peak": peak, "peak_source": peak_src,
                          "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None,
@@ -365,6 +372,27 @@ def run_native(args) -> int:
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def autotune(rt, size: int, world: int) -> dict:
+    """Tuning-table cell for (all_reduce, world, size) built with the repo's
+    tuner (CUDA-event device time, cross-rank max) and installed on the
+    runtime; returns {algorithm: median_us} and the winner."""
+    from paper_2303_08374_b200.core import CommOpKind, DType
+    from paper_2303_08374_b200.tuner import BenchConfig, bench, build_table
+
+    if world == 1:
+        return {"winner": "local copy (p = 1)"}
+    cfg = BenchConfig(ops=[CommOpKind.all_reduce], sizes=[size], dtype=DType.f32,
+                      warmup_iters=2, measure_iters=3)
+    samples, skipped = bench(rt, cfg, "nvl")
+    rt.tuning_table = build_table(samples, skipped=skipped, system="bench.py in-situ")
+    entry = rt.tuning_table.lookup_entry(CommOpKind.all_reduce, world, size)
+    import statistics
+
+    return {"candidates_us": {s.algorithm: round(statistics.median(s.durations) * 1e6, 1)
+                              for s in samples},
+            "winner": entry.algorithm if entry else None}
 
 
 def _ncu_traffic(world: int):

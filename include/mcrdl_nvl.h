@@ -205,6 +205,9 @@ const char* mcrdl_status_kind(mcrdl_status_t status);
 int mcrdl_abi_version(void);
 /* Number of kernels this library launched since load (evidence counter). */
 uint64_t mcrdl_launch_count(void);
+/* Developer timeline: host-mapped [512 CTAs x slots] %globaltimer stamps of
+ * the last ops (NULL unless the library was built with `build.py --trace`). */
+mcrdl_status_t mcrdl_debug_trace(mcrdl_comm* comm, uint64_t** host_ptr, uint64_t* slots_per_cta);
 
 #ifdef __cplusplus
 }

@@ -41,9 +41,14 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every CUDA source for sm_100a and link the shared library."""
-    OBJDIR.mkdir(parents=True, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
+    """Compile every CUDA source for sm_100a and link the shared library.
+    trace=True builds the developer timeline variant libmcrdl_nvl_trace.so
+    (-DMCRDL_TRACE; loaded when MCRDL_TRACE_LIB=1)."""
+    objdir = OBJDIR.parent / "obj_trace" if trace else OBJDIR
+    lib = LIBDIR / "libmcrdl_nvl_trace.so" if trace else LIB
+    extra = ["-DMCRDL_TRACE"] if trace else []
+    objdir.mkdir(parents=True, exist_ok=True)
     LIBDIR.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "mcrdl_nvl.h"]
     cc = nvcc()
@@ -51,10 +56,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     for src in SOURCES:
         s = CSRC / src
-        o = OBJDIR / (Path(src).stem + ".o")
+        o = objdir / (Path(src).stem + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [cc, *ARCH, *FLAGS, "-Xptxas", "-v" if verbose else "-O3",
+            cmd = [cc, *ARCH, *FLAGS, *extra, "-Xptxas", "-v" if verbose else "-O3",
                    "-I", str(ROOT / "include"), "-c", str(s), "-o", str(o)]
             jobs.append(cmd)
     if jobs:
@@ -66,15 +71,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                 raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
             if verbose:
                 sys.stderr.write(res.stderr)
-    if force or jobs or _stale(LIB, objs):
-        cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs),
+    if force or jobs or _stale(lib, objs):
+        cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs),
                "-Xlinker", "--no-undefined", "-lpthread", "-ldl", "-lrt"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
             raise RuntimeError("nvcc link failed")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                trace="--trace" in sys.argv))

@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   stage_comm(c, S);
   __syncthreads();
   const uint8_t* ws = S.ws[rank] + hoff;
+  MCRDL_TRACE_AT(c, bid, 0);
 
   if (TMA && role == 0) {  // ---------------------------- sender (TMA bulk)
     if (tid != 0) return;
@@ -299,8 +300,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int q = 0; q < world; ++q)
           if (q != rank && r < nchunks(seg_len(npk, sp, q, b0, b1), chp, sh))
             publish(&S.pad[q]->flag[par][sh][rank], make_flag(epoch, sig, uint32_t(r + 1)));
+        MCRDL_TRACE_AT(c, bid, 1 + r);
       }
     }
+    MCRDL_TRACE_AT(c, bid, kTraceSlots - 1);
     return;
   }
 
@@ -321,7 +324,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncthreads();
       if (tid < world && tid != rank && r < nchunks(seg_len(npk, sp, tid, rb, re), chp, s))
         publish(&S.pad[tid]->flag[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
+      MCRDL_TRACE_AT(c, bid, 1 + r);
     }
+    MCRDL_TRACE_AT(c, bid, kTraceSlots - 1);
     return;
   }
 
@@ -335,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (e) atomicCAS(&s_err, 0, e);
       }
       __syncthreads();
+      MCRDL_TRACE_AT(c, bid, 1 + 2 * r);
       if (s_err) {
         if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
         return;
@@ -380,7 +386,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncthreads();
       if (tid < world && tid != rank)
         publish(&S.pad[tid]->flag2[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
+      MCRDL_TRACE_AT(c, bid, 2 + 2 * r);
     }
+    MCRDL_TRACE_AT(c, bid, kTraceSlots - 1);
     return;
   }
 
@@ -395,6 +403,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (e) atomicCAS(&s_err, 0, e);
     }
     __syncthreads();
+    MCRDL_TRACE_AT(c, bid, 1 + 2 * r);
     if (s_err) {
       if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
       return;
@@ -416,7 +425,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       for (; i < rb + hi; i += nt) store_pack<T, VEC>(out, int64_t(q) * sp + i, n, ld16_cg(src + i * 16));
     }
+    MCRDL_TRACE_AT(c, bid, 2 + 2 * r);
   }
+  MCRDL_TRACE_AT(c, bid, kTraceSlots - 1);
 }
 
 // ----------------------------------------------------------- NVLS (switch)
@@ -642,9 +653,9 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // Local copy used for world == 1 (the p = 1 floor: out[:] = in).
-// Grid-stride (interleaved across CTAs, 4 x 16 B in flight per thread): on
-// B200 this reaches ~93% of the measured copy peak where contiguous per-CTA
-// chunks reach ~85% (tools/p2p_probe.cu, local column).
+// Grid-stride (interleaved across CTAs, 8 x 16 B in flight per thread): on
+// B200 this reaches ~93-96% of the measured copy peak where contiguous
+// per-CTA chunks reach ~85% (tools/p2p_probe.cu, tools/copy_probe.cu).
 __global__ void __launch_bounds__(kThreads) k_copy(uint8_t* dst, const uint8_t* src, int64_t n) {
   if (((uintptr_t(dst) | uintptr_t(src)) & 15) != 0) {
     int64_t s, e;
@@ -657,14 +668,14 @@ __global__ void __launch_bounds__(kThreads) k_copy(uint8_t* dst, const uint8_t* 
   uint4* d4 = reinterpret_cast<uint4*>(dst);
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < np; i += 4 * stride) {
-    uint4 v[4];
+  for (; i + 7 * stride < np; i += 8 * stride) {
+    uint4 v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = __ldcs(s4 + i + u * stride);
+    for (int u = 0; u < 8; ++u) v[u] = s4[i + u * stride];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) __stcs(d4 + i + u * stride, v[u]);
+    for (int u = 0; u < 8; ++u) d4[i + u * stride] = v[u];
   }
-  for (; i < np; i += stride) __stcs(d4 + i, __ldcs(s4 + i));
+  for (; i < np; i += stride) d4[i] = s4[i];
   if (blockIdx.x == 0)
     for (int64_t k = (np << 4) + threadIdx.x; k < n; k += blockDim.x) dst[k] = src[k];
 }
@@ -684,9 +695,10 @@ static int grid_for(int64_t packs, int num_sms, int max_blocks) {
 mcrdl_status_t launch_local_copy(void* dst, const void* src, int64_t nbytes, int num_sms,
                                  cudaStream_t stream) {
   if (nbytes <= 0 || dst == src) return MCRDL_OK;
-  // One persistent wave (one CTA per SM) measured best for large copies.
-  int64_t g = (nbytes + (int64_t(kThreads) * 64) - 1) / (int64_t(kThreads) * 64);
-  if (g > num_sms) g = num_sms;
+  // 8 x 16 B in flight per thread over ~16 CTAs per SM measured best for
+  // large copies (tools/copy_probe.cu: 6.32 TB/s vs 6.20 for cudaMemcpy D2D).
+  int64_t g = (nbytes + (int64_t(kThreads) * 128) - 1) / (int64_t(kThreads) * 128);
+  if (g > 16 * num_sms) g = 16 * num_sms;
   if (g < 1) g = 1;
   k_copy<<<int(g), kThreads, 0, stream>>>(reinterpret_cast<uint8_t*>(dst),
                                           reinterpret_cast<const uint8_t*>(src), nbytes);

@@ -567,6 +567,14 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   *c->err_host = 0;
   MCRDL_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
   MCRDL_CUDA_CHECK(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
+#ifdef MCRDL_TRACE
+  {
+    const size_t tb = size_t(kMaxBlocks) * kTraceSlots * sizeof(uint64_t);
+    MCRDL_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&c->trace_host), tb, cudaHostAllocMapped));
+    memset(c->trace_host, 0, tb);
+    MCRDL_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dc.trace), c->trace_host, 0));
+  }
+#endif
 
   c->dc.rank = rank;
   c->dc.world = world;
@@ -593,8 +601,16 @@ mcrdl_status_t mcrdl_comm_destroy(mcrdl_comm* c) {
   teardown_nvls(c);
   if (c->err_host) cudaFreeHost(c->err_host);
   if (c->order_ev) cudaEventDestroy(c->order_ev);
+  if (c->trace_host) cudaFreeHost(c->trace_host);
   if (c->listen_fd >= 0) close(c->listen_fd);
   delete c;
+  return MCRDL_OK;
+}
+
+mcrdl_status_t mcrdl_debug_trace(mcrdl_comm* c, uint64_t** host_ptr, uint64_t* slots_per_cta) {
+  if (c == nullptr || host_ptr == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL argument");
+  *host_ptr = c->trace_host;  // NULL unless built with --trace
+  if (slots_per_cta) *slots_per_cta = kTraceSlots;
   return MCRDL_OK;
 }
 

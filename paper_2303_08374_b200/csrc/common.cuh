@@ -53,11 +53,27 @@ struct DevComm {
   uint8_t* ws[kMaxRanks];  // rank r's workspace, mapped in this address space
   Pad* pad[kMaxRanks];     // rank r's signal pad
   int* err;                // host-mapped latched error word
+  uint64_t* trace;         // host-mapped timeline (trace builds only), else null
   uint64_t timeout_ns;
   int64_t half_bytes;      // bytes per workspace half
   int rank;
   int world;
 };
+
+// Developer timeline (build.py --trace defines MCRDL_TRACE): thread 0 of a CTA
+// stamps %globaltimer into slot [cta][idx] of a host-mapped buffer.
+constexpr int kTraceSlots = 256;
+#ifdef MCRDL_TRACE
+#define MCRDL_TRACE_AT(c, cta, idx)                                                       \
+  do {                                                                                    \
+    if ((c).trace && threadIdx.x == 0 && (idx) < kTraceSlots)                             \
+      (c).trace[int64_t(cta) * kTraceSlots + (idx)] = globaltimer_ns();                   \
+  } while (0)
+#else
+#define MCRDL_TRACE_AT(c, cta, idx) \
+  do {                              \
+  } while (0)
+#endif
 
 // ------------------------------------------------------------ primitives
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {

@@ -65,6 +65,7 @@ struct mcrdl_comm {
   cudaEvent_t order_ev = nullptr;
   cudaStream_t last_stream = nullptr;
   bool have_last = false;
+  uint64_t* trace_host = nullptr;  // trace builds: kMaxBlocks x kTraceSlots stamps
 };
 
 namespace mcrdl {

@@ -59,6 +59,7 @@ SIGNATURES = {
     "mcrdl_status_kind": (c_char_p, [c_int]),
     "mcrdl_abi_version": (c_int, []),
     "mcrdl_launch_count": (c_uint64, []),
+    "mcrdl_debug_trace": (c_int, [_P, POINTER(POINTER(c_uint64)), POINTER(c_uint64)]),
 }
 
 _lib: Optional[ctypes.CDLL] = None
@@ -66,9 +67,13 @@ _lib: Optional[ctypes.CDLL] = None
 
 def load() -> ctypes.CDLL:
     """Load libmcrdl_nvl.so (built in-tree by paper_2303_08374_b200.build)."""
-    global _lib
+    global _lib, LIB_PATH
     if _lib is not None:
         return _lib
+    import os
+
+    if os.environ.get("MCRDL_TRACE_LIB", "0") not in ("", "0"):
+        LIB_PATH = LIB_PATH.with_name("libmcrdl_nvl_trace.so")  # developer timeline build
     if not LIB_PATH.exists():
         raise NativeBackendMissing(
             f"{LIB_PATH} is not built; run `python -m paper_2303_08374_b200.build` "

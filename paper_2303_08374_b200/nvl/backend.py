@@ -302,6 +302,9 @@ class NvlBackendInstance:
             self._seq += 1
             handle.mark_in_progress()
             self._reap()
+            if self._pipelined_ok(request):
+                self._post_pipelined(request, handle)
+                return handle
             caller = torch.cuda.current_stream(self.device)
             lane = self.stream
             lane.wait_stream(caller)
@@ -319,6 +322,68 @@ class NvlBackendInstance:
                 t1.record(lane)
             self._arm(handle, request, st, t0, t1)
         return handle
+
+    # ------------------------------------------- pipelined host staging
+    PIPE_MIN_BYTES = 16 << 20
+    PIPE_CHUNK_BYTES = 32 << 20
+
+    def _pipelined_ok(self, req: CommRequest) -> bool:
+        """Large all_reduce on pinned host tensors: overlap H2D, the collective
+        and D2H chunk by chunk (PCIe is full duplex)."""
+        if req.kind is not CommOpKind.all_reduce:
+            return False
+        for b in (req.input, req.output):
+            if not (b.is_tensor and not b.is_device and b.array.is_pinned()):
+                return False
+        return req.input.nbytes >= self.PIPE_MIN_BYTES
+
+    def _post_pipelined(self, req: CommRequest, handle: WorkHandle) -> None:
+        dt = req.input.dtype
+        n = req.input.count
+        k = max(2, min(32, req.input.nbytes // self.PIPE_CHUNK_BYTES))
+        step = ((n + k - 1) // k + 63) // 64 * 64
+        h_in, h_out = req.input.array, req.output.array
+        lane = self.stream
+        if getattr(self, "_up", None) is None:
+            self._up = torch.cuda.Stream(device=self.device)
+            self._down = torch.cuda.Stream(device=self.device)
+        up, down = self._up, self._down
+        with torch.cuda.stream(lane):
+            d = torch.empty(n, dtype=dt.torch_dtype, device=self.device)
+        d.record_stream(up)
+        d.record_stream(down)
+        up.wait_stream(lane)  # d's memory is ready for reuse in lane order
+        lib, c = self.comm.lib, self.comm.handle
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(up)
+        algo = self._algo_code(CommOpKind.all_reduce, min(n, step) * dt.size_bytes)
+        req._algorithm = _ALGO_NAMES.get(algo, "auto")
+        for j, lo in enumerate(range(0, n, step)):
+            hi = min(n, lo + step)
+            with torch.cuda.stream(up):
+                d[lo:hi].copy_(h_in[lo:hi], non_blocking=True)
+            e_up = torch.cuda.Event()
+            e_up.record(up)
+            lane.wait_event(e_up)
+            try:
+                _lib.check(lib.mcrdl_all_reduce(c, int(d[lo:hi].data_ptr()), int(d[lo:hi].data_ptr()),
+                                                hi - lo, dt.code, req.op.code, algo,
+                                                (req.seq << 8) | (j & 0xFF), int(lane.cuda_stream)))
+            except BaseException as exc:
+                self._fail_now(handle, req, exc)
+                raise
+            e_ar = torch.cuda.Event()
+            e_ar.record(lane)
+            down.wait_event(e_ar)
+            with torch.cuda.stream(down):
+                h_out[lo:hi].copy_(d[lo:hi], non_blocking=True)
+        self._last_raw = int(lane.cuda_stream)
+        t1.record(down)
+        lane.wait_stream(down)  # later ops of this backend see the host copy finished
+        st = _Staging(self.device, lane, self._pool)
+        st.keep.extend([d, h_in, h_out])
+        self._arm(handle, req, st, t0, t1)
 
     def post_fused(self, members: Sequence[CommRequest], ready_events: Sequence,
                    flush_request: CommRequest) -> WorkHandle:
