@@ -135,6 +135,15 @@ mcrdl_status_t mcrdl_all_reduce(mcrdl_comm* comm, const void* in, void* out, uin
                                 mcrdl_dtype_t dtype, mcrdl_redop_t op, mcrdl_algo_t algo,
                                 uint64_t seq, void* stream);
 
+/* reduce_scatter (runtime.py:590-597; collectives.py:609-645; oracle
+ * reference.py:79-83): in holds world*recvcount elements, rank r receives the
+ * ascending-fold reduction of segment r. Needs 16-byte aligned buffers and
+ * recvcount*esize % 16 == 0 within one workspace half, else
+ * MCRDL_ERR_UNSUPPORTED (compose all_reduce + slice). */
+mcrdl_status_t mcrdl_reduce_scatter(mcrdl_comm* comm, const void* in, void* out, uint64_t recvcount,
+                                    mcrdl_dtype_t dtype, mcrdl_redop_t op, mcrdl_algo_t algo,
+                                    uint64_t seq, void* stream);
+
 /* all_to_allv (runtime.py:616-626; collectives.py:648-733). Counts and
  * displacements are in ELEMENTS. Host-array form: four arrays of `world`
  * int64 values on the host (passed by value into the kernel; no H2D copy). */

@@ -242,7 +242,7 @@ __device__ __forceinline__ void tma_drain() {
 template <typename T, int OP, bool VEC, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2)
     k_ar_pipe(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp, int gs,
-              int64_t chp, uint32_t epoch, uint32_t sig) {
+              int64_t chp, uint32_t epoch, uint32_t sig, T* rs_out = nullptr, int64_t rs_n = 0) {
   constexpr int N = Pack<T>::N;
   __shared__ int s_err;
   __shared__ SComm S;
@@ -376,6 +376,10 @@ __global__ void __launch_bounds__(kThreads, 2)
           const int64_t i = i0 + u * nt;
           if (i >= rb + hi) break;
           const uint4 res = acc[u].to_raw();
+          if (rs_out != nullptr) {  // reduce_scatter: my segment is my output
+            store_pack<T, VEC>(rs_out, i, rs_n, res);
+            continue;
+          }
           for (int k = 1; k < world; ++k) {
             const int q = (rank + k) % world;
             st16(S.ws[q] + hoff + ag + int64_t(rank) * segb + i * 16, res);
@@ -383,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           store_pack<T, VEC>(out, int64_t(rank) * sp + i, n, res);
         }
       }
+      if (rs_out != nullptr) continue;
       __syncthreads();
       if (tid < world && tid != rank)
         publish(&S.pad[tid]->flag2[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
@@ -393,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 
   // ------------------------------------------------------------- gatherer
+  if (rs_out != nullptr) return;  // reduce_scatter has no all-gather phase
   int rows = 0;
   for (int q = 0; q < world; ++q)
     if (q != rank) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
@@ -428,6 +434,175 @@ __global__ void __launch_bounds__(kThreads, 2)
     MCRDL_TRACE_AT(c, bid, 2 + 2 * r);
   }
   MCRDL_TRACE_AT(c, bid, kTraceSlots - 1);
+}
+
+// ------------------------------------- warp-specialized two-shot (K2, v3)
+// Same three roles as k_ar_pipe, but inside EVERY CTA as warp groups
+// (senders | reducers | gatherers) synchronised with named barriers, one
+// share per CTA. Measured with tools/trace_ar.py: when roles are whole CTAs,
+// the SMs they share are loaded unevenly and the slowest static share sets
+// the op time (p=2: sender row time p10 56 us vs p90 100 us). Here every SM
+// carries the same mix and the groups never wait for each other locally, only
+// for their peers' flags.
+template <int WS, int WR>
+struct WsRoles {
+  static constexpr int kSend = WS * 32, kRed = WR * 32, kGath = kThreads - (WS + WR) * 32;
+};
+
+template <typename T, bool VEC>
+__device__ __forceinline__ void push_packs_g(const T* in, int64_t n, int64_t g0, int64_t cnt,
+                                             uint8_t* dst, int gtid, int gnt) {
+  int64_t i = gtid;
+  for (; i + 3 * gnt < cnt; i += 4 * gnt) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = load_pack<T, VEC>(in, g0 + i + u * gnt, n);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) st16(dst + (i + u * gnt) * 16, v[u]);
+  }
+  for (; i < cnt; i += gnt) st16(dst + i * 16, load_pack<T, VEC>(in, g0 + i, n));
+}
+
+template <typename T, int OP, bool VEC>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_ar_ws(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int64_t chp,
+            uint32_t epoch, uint32_t sig) {
+  constexpr int N = Pack<T>::N;
+  constexpr int WS = 6, WR = 6;
+  using Roles = WsRoles<WS, WR>;
+  __shared__ int s_gerr[3];  // per group: written by the group's waiters before its barrier
+  __shared__ SComm S;
+  const int par = epoch & 1, rank = c.rank, world = c.world;
+  const int warp = int(threadIdx.x) >> 5;
+  const int role = warp < WS ? 0 : (warp < WS + WR ? 1 : 2);
+  const int gbase = role == 0 ? 0 : (role == 1 ? Roles::kSend : Roles::kSend + Roles::kRed);
+  const int gnt = role == 0 ? Roles::kSend : (role == 1 ? Roles::kRed : Roles::kGath);
+  const int gtid = int(threadIdx.x) - gbase;
+  const int bar_id = 1 + role;
+  const int s = blockIdx.x, gp = gridDim.x;
+  const int64_t npk = (n + N - 1) / N;
+  const int64_t rb = sp * s / gp, re = sp * (s + 1) / gp;
+  const int64_t hoff = int64_t(par) * c.half_bytes;
+  const int64_t ag = int64_t(world) * segb;
+  if (threadIdx.x < 3) s_gerr[threadIdx.x] = 0;
+  stage_comm(c, S);
+  __syncthreads();  // the last barrier shared by all roles
+  const uint8_t* ws = S.ws[rank] + hoff;
+  MCRDL_TRACE_AT(c, s, 0);
+  auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(gnt) : "memory"); };
+  volatile int* verr = &s_gerr[role];
+  int* s_err_p = &s_gerr[role];
+
+  if (role == 0) {  // ------------------------------------------ senders
+    int rows = 0;
+    for (int q = 0; q < world; ++q)
+      if (q != rank) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
+    for (int r = 0; r < rows; ++r) {
+      for (int k = 1; k < world; ++k) {
+        const int q = (rank + k) % world;
+        const int64_t len = seg_len(npk, sp, q, rb, re);
+        const int64_t lo = int64_t(r) * chp;
+        if (lo >= len) continue;
+        push_packs_g<T, VEC>(in, n, int64_t(q) * sp + rb + lo, min(chp, len - lo),
+                             S.ws[q] + hoff + int64_t(rank) * segb + (rb + lo) * 16, gtid, gnt);
+      }
+      gsync();
+      if (gtid < world && gtid != rank && r < nchunks(seg_len(npk, sp, gtid, rb, re), chp, s))
+        publish(&S.pad[gtid]->flag[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
+    }
+    return;
+  }
+
+  if (role == 1) {  // ----------------------------------------- reducers
+    const int64_t len = seg_len(npk, sp, rank, rb, re);
+    const int rows = nchunks(len, chp, s);
+    for (int r = 0; r < rows; ++r) {
+      if (gtid < world && gtid != rank) {
+        int e = wait_flag(&S.pad[rank]->flag[par][s][gtid], S.pad[rank], c.timeout_ns, c.err, epoch,
+                          sig, uint32_t(r + 1));
+        if (e) atomicCAS(s_err_p, 0, e);
+      }
+      gsync();
+      if (*verr) {
+        if (gtid == 0) raise_error(S.pad, world, c.err, *verr, epoch);
+        return;
+      }
+      const int64_t lo = int64_t(r) * chp, hi = min(len, lo + chp);
+      constexpr int RU = sizeof(T) == 2 ? 2 : 4;
+      for (int64_t i0 = rb + lo + gtid; i0 < rb + hi; i0 += RU * gnt) {
+        Pack<T> acc[RU];
+        uint4 v[RU];
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const int64_t i = i0 + u * gnt;
+          if (i < rb + hi)
+            v[u] = rank == 0 ? load_pack<T, VEC>(in, int64_t(rank) * sp + i, n) : ld16_cg(ws + i * 16);
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) acc[u].from_raw(v[u]);
+        for (int q = 1; q < world; ++q) {
+#pragma unroll
+          for (int u = 0; u < RU; ++u) {
+            const int64_t i = i0 + u * gnt;
+            if (i < rb + hi)
+              v[u] = (q == rank) ? load_pack<T, VEC>(in, int64_t(rank) * sp + i, n)
+                                 : ld16_cg(ws + int64_t(q) * segb + i * 16);
+          }
+#pragma unroll
+          for (int u = 0; u < RU; ++u) acc[u].template fold<OP>(v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const int64_t i = i0 + u * gnt;
+          if (i >= rb + hi) break;
+          const uint4 res = acc[u].to_raw();
+          for (int k = 1; k < world; ++k) {
+            const int q = (rank + k) % world;
+            st16(S.ws[q] + hoff + ag + int64_t(rank) * segb + i * 16, res);
+          }
+          store_pack<T, VEC>(out, int64_t(rank) * sp + i, n, res);
+        }
+      }
+      gsync();
+      if (gtid < world && gtid != rank)
+        publish(&S.pad[gtid]->flag2[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ gatherers
+  int rows = 0;
+  for (int q = 0; q < world; ++q)
+    if (q != rank) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
+  for (int r = 0; r < rows; ++r) {
+    if (gtid < world && gtid != rank && r < nchunks(seg_len(npk, sp, gtid, rb, re), chp, s)) {
+      int e = wait_flag(&S.pad[rank]->flag2[par][s][gtid], S.pad[rank], c.timeout_ns, c.err, epoch,
+                        sig, uint32_t(r + 1));
+      if (e) atomicCAS(s_err_p, 0, e);
+    }
+    gsync();
+    if (*verr) {
+      if (gtid == 0) raise_error(S.pad, world, c.err, *verr, epoch);
+      return;
+    }
+    for (int k = 1; k < world; ++k) {
+      const int q = (rank + k) % world;
+      const int64_t len = seg_len(npk, sp, q, rb, re);
+      const int64_t lo = int64_t(r) * chp;
+      if (lo >= len) continue;
+      const int64_t hi = min(len, lo + chp);
+      const uint8_t* src = ws + ag + int64_t(q) * segb;
+      int64_t i = rb + lo + gtid;
+      for (; i + 3 * gnt < rb + hi; i += 4 * gnt) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ld16_cg(src + (i + u * gnt) * 16);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) store_pack<T, VEC>(out, int64_t(q) * sp + i + u * gnt, n, v[u]);
+      }
+      for (; i < rb + hi; i += gnt) store_pack<T, VEC>(out, int64_t(q) * sp + i, n, ld16_cg(src + i * 16));
+    }
+  }
 }
 
 // ----------------------------------------------------------- NVLS (switch)
@@ -810,7 +985,23 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
         static const int64_t tma_on = env_int("MCRDL_AR_TMA", 1);
         static const int64_t tma_ctas = env_int("MCRDL_AR_TMA_CTAS", 64);
         const bool big = m * int64_t(sizeof(T)) >= (int64_t(256) << 20);
-        if (vec && (tma_on == 2 || (tma_on == 1 && big))) {
+        // Warp-specialized kernel (one share per CTA, all roles per CTA):
+        // MCRDL_AR_KERNEL=1 selects it, 0 the CTA-role kernels below.
+        // Measured (tools/ws_ab.sh): p=2 +2%, p=4 -9% at 256 MiB -> default off.
+        static const int64_t ws_kernel = env_int("MCRDL_AR_KERNEL", 0);
+        int64_t gw = (sp * 16 + (32 << 10) - 1) / (32 << 10);
+        gw = std::max<int64_t>(1, std::min<int64_t>(gw, std::min<int64_t>(2 * c->num_sms, kMaxBlocks)));
+        const int64_t sharew = (sp + gw - 1) / gw;
+        int64_t chpw = (sharew + 3999) / 4000;
+        if (chpw < chunk_kb * 64) chpw = chunk_kb * 64;
+        if (ws_kernel == 1) {
+          if (vec)
+            k_ar_ws<T, OP, true><<<int(gw), kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, chpw,
+                                                                   epoch, sig);
+          else
+            k_ar_ws<T, OP, false><<<int(gw), kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, chpw,
+                                                                    epoch, sig);
+        } else if (vec && (tma_on == 2 || (tma_on == 1 && big))) {
           const int gs = int(std::min<int64_t>(gp, tma_ctas));
           int64_t gpt = gp;
           const int64_t cap = (2 * c->num_sms - gs) / 2;  // gs + 2*gp <= 2 CTAs/SM
@@ -850,6 +1041,52 @@ static mcrdl_status_t ar_op(mcrdl_comm* c, const void* in, void* out, int64_t n,
     case MCRDL_PROD: return ar_typed<T, MCRDL_PROD>(c, i, o, n, algo, seq, dt, s);
     case MCRDL_MIN: return ar_typed<T, MCRDL_MIN>(c, i, o, n, algo, seq, dt, s);
     case MCRDL_MAX: return ar_typed<T, MCRDL_MAX>(c, i, o, n, algo, seq, dt, s);
+  }
+  return set_error(MCRDL_ERR_VALIDATION, "unknown reduce op %d", int(op));
+}
+
+// reduce_scatter (reference _reduce_scatter_ring/_naive, collectives.py:609-645):
+// the RS half of the two-shot pipeline; rank r's reduced segment (ascending
+// fold, bit-exact) lands straight in its m-element output. Needs 16-byte
+// aligned buffers, m*sizeof(T) % 16 == 0 and one workspace half; otherwise
+// MCRDL_ERR_UNSUPPORTED (the caller composes all_reduce + slice).
+template <typename T, int OP>
+static mcrdl_status_t rs_typed(mcrdl_comm* c, const T* in, T* out, int64_t m, uint64_t seq, int dt,
+                               cudaStream_t stream) {
+  const int world = c->world;
+  if (world == 1) return launch_local_copy(out, in, m * int64_t(sizeof(T)), c->num_sms, stream);
+  const int64_t segbytes = m * int64_t(sizeof(T));
+  if (((uintptr_t(in) | uintptr_t(out)) & 15) != 0 || segbytes % 16 != 0 ||
+      2 * int64_t(world) * ((segbytes + 255) / 256 * 256) > c->dc.half_bytes)
+    return set_error(MCRDL_ERR_UNSUPPORTED, "reduce_scatter kernel needs aligned 16-byte segments "
+                                            "within one workspace half");
+  uint32_t epoch;
+  mcrdl_status_t st = begin_op(c, stream, &epoch);
+  if (st != MCRDL_OK) return st;
+  const uint32_t sig = op_sig(kKindReduceScatter, dt, OP, -1, uint64_t(m), seq);
+  const int64_t sp = segbytes / 16;
+  const int64_t segb = (sp * 16 + 255) / 256 * 256;
+  int64_t gp = (segbytes + (32 << 10) - 1) / (32 << 10);
+  gp = std::max<int64_t>(1, std::min<int64_t>(gp, 2 * c->num_sms / 3));
+  int64_t chp = ((sp + gp - 1) / gp + 3999) / 4000;
+  if (chp < 16384) chp = 16384;
+  k_ar_pipe<T, OP, true, false><<<int(3 * gp), kThreads, 0, stream>>>(
+      c->dc, in, out, int64_t(world) * m, sp, segb, int(gp), int(gp), chp, epoch, sig, out, m);
+  count_launch();
+  MCRDL_CUDA_CHECK(cudaGetLastError());
+  return MCRDL_OK;
+}
+
+template <typename T>
+static mcrdl_status_t rs_op(mcrdl_comm* c, const void* in, void* out, int64_t m, mcrdl_redop_t op,
+                            uint64_t seq, int dt, cudaStream_t s) {
+  const T* i = reinterpret_cast<const T*>(in);
+  T* o = reinterpret_cast<T*>(out);
+  switch (op) {
+    case MCRDL_SUM: return rs_typed<T, MCRDL_SUM>(c, i, o, m, seq, dt, s);
+    case MCRDL_PROD: return rs_typed<T, MCRDL_PROD>(c, i, o, m, seq, dt, s);
+    case MCRDL_MIN: return rs_typed<T, MCRDL_MIN>(c, i, o, m, seq, dt, s);
+    case MCRDL_MAX: return rs_typed<T, MCRDL_MAX>(c, i, o, m, seq, dt, s);
   }
   return set_error(MCRDL_ERR_VALIDATION, "unknown reduce op %d", int(op));
 }
@@ -911,6 +1148,26 @@ mcrdl_status_t mcrdl_all_reduce(mcrdl_comm* c, const void* in, void* out, uint64
     case MCRDL_I64: return ar_op<int64_t>(c, in, out, n, op, algo, seq, int(dtype), s);
     case MCRDL_U8: return ar_op<uint8_t>(c, in, out, n, op, algo, seq, int(dtype), s);
     case MCRDL_BF16: return ar_op<__nv_bfloat16>(c, in, out, n, op, algo, seq, int(dtype), s);
+  }
+  return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+}
+
+mcrdl_status_t mcrdl_reduce_scatter(mcrdl_comm* c, const void* in, void* out, uint64_t recvcount,
+                                    mcrdl_dtype_t dtype, mcrdl_redop_t op, mcrdl_algo_t algo,
+                                    uint64_t seq, void* stream) {
+  (void)algo;
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  if (recvcount == 0) return mcrdl_barrier(c, seq, stream);
+  if (in == nullptr || out == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL buffer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t m = int64_t(recvcount);
+  switch (dtype) {
+    case MCRDL_F32: return rs_op<float>(c, in, out, m, op, seq, int(dtype), s);
+    case MCRDL_F64: return rs_op<double>(c, in, out, m, op, seq, int(dtype), s);
+    case MCRDL_I32: return rs_op<int32_t>(c, in, out, m, op, seq, int(dtype), s);
+    case MCRDL_I64: return rs_op<int64_t>(c, in, out, m, op, seq, int(dtype), s);
+    case MCRDL_U8: return rs_op<uint8_t>(c, in, out, m, op, seq, int(dtype), s);
+    case MCRDL_BF16: return rs_op<__nv_bfloat16>(c, in, out, m, op, seq, int(dtype), s);
   }
   return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
 }

@@ -123,6 +123,7 @@ enum KindTag : int {
   kKindA2ASingle = 12,
   kKindA2AList = 13,
   kKindA2AV = 14,
+  kKindReduceScatter = 11,
   kKindBarrier = 99,
 };
 

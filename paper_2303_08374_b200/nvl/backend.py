@@ -542,10 +542,15 @@ class NvlBackendInstance:
                                          seq, s))
             else:
                 m = req.output.count
-                full = st.scratch(p * m, dt)
-                chk(lib.mcrdl_all_reduce(c, _ptr(i), _ptr(full), p * m, dt.code, op, algo, seq, s))
                 o = st.dev(req.output, upload=False, download=True)
-                o.copy_(full[rank * m:(rank + 1) * m])
+                rc = lib.mcrdl_reduce_scatter(c, _ptr(i), _ptr(o), m, dt.code, op, algo, seq, s)
+                if rc == 4:  # kernel declined (alignment / size): compose on the device
+                    full = st.scratch(p * m, dt)
+                    chk(lib.mcrdl_all_reduce(c, _ptr(i), _ptr(full), p * m, dt.code, op, algo, seq,
+                                             s))
+                    o.copy_(full[rank * m:(rank + 1) * m])
+                else:
+                    chk(rc)
             return
 
         if kind is CommOpKind.bcast:

@@ -309,11 +309,18 @@ def sc_reduce_family(cx: Ctx):
             cx.check(f"reduce/root{root}", from_dev(t, DType.f32), seqref.fold(ins, "sum"))
         else:
             cx.check(f"reduce/nonroot-untouched/{root}", from_dev(t, DType.f32), ins[r])
-    m = 1001
-    ins = [values(DType.i64, p * m, "rs", q) for q in range(p)]
-    o = torch.zeros(m, dtype=torch.int64, device=cx.dev)
-    cx.rt.reduce_scatter(cx.b, Buffer(o), Buffer(to_dev(ins[r], DType.i64, cx.dev)))
-    cx.check("reduce_scatter", from_dev(o, DType.i64), seqref.reduce_scatter(ins, "sum")[r])
+    # composed path (m*8 % 16 != 0) and the native RS kernel (aligned segments)
+    for dtype, m, op in ((DType.i64, 1001, "sum"), (DType.f32, 1 << 16, "sum"),
+                         (DType.bf16, 4096, "sum"), (DType.i32, 12288, "max"),
+                         (DType.f32, (3 << 20) + 4, "sum")):
+        ins = [values(dtype, p * m, "rs", dtype.name, m, q) for q in range(p)]
+        o = torch.zeros(m, dtype=dtype.torch_dtype, device=cx.dev)
+        cx.rt.reduce_scatter(cx.b, Buffer(o), Buffer(to_dev(ins[r], dtype, cx.dev)), ReduceOp(op))
+        if dtype is DType.bf16:
+            want = seqref.fold_bf16([x[r * m:(r + 1) * m] for x in ins], op)
+        else:
+            want = seqref.reduce_scatter(ins, op)[r]
+        cx.check(f"reduce_scatter/{dtype.name}/{m}/{op}", from_dev(o, dtype), want)
 
 
 def sc_host_buffers(cx: Ctx):
