@@ -18,8 +18,7 @@ namespace mcrdl {
 // peer's workspace slot `rank`; phase 2 folds slots 0..p-1 (own input for
 // slot == rank) into `out`. Latency: one NVLink write + one flag per peer.
 template <typename T, int OP, bool VEC>
-__global__ void __launch_bounds__(kThreads)
-    k_ar_oneshot(DevComm c, const T* in, T* out, int64_t n, int64_t slot_bytes, uint32_t epoch,
+__device__ __forceinline__ void ar_oneshot_body(DevComm c, const T* in, T* out, int64_t n, int64_t slot_bytes, uint32_t epoch,
                  uint32_t sig) {
   constexpr int N = Pack<T>::N;
   __shared__ int s_err;
@@ -65,6 +64,13 @@ __global__ void __launch_bounds__(kThreads)
     }
     store_pack<T, VEC>(out, i, n, acc.to_raw());
   }
+}
+
+template <typename T, int OP, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_ar_oneshot(DevComm c, const T* in, T* out, int64_t n, int64_t slot_bytes, uint32_t sig) {
+  const uint32_t epoch = epoch_enter(c);
+  ar_oneshot_body<T, OP, VEC>(c, in, out, n, slot_bytes, epoch, sig);
+  epoch_exit(c, epoch);
 }
 
 // ------------------------------------------------ pipelined two-shot (K2)
@@ -240,9 +246,8 @@ __device__ __forceinline__ void tma_drain() {
 }
 
 template <typename T, int OP, bool VEC, bool TMA>
-__global__ void __launch_bounds__(kThreads, 2)
-    k_ar_pipe(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp, int gs,
-              int64_t chp, uint32_t epoch, uint32_t sig, T* rs_out = nullptr, int64_t rs_n = 0) {
+__device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp, int gs,
+              int64_t chp, uint32_t epoch, uint32_t sig, T* rs_out, int64_t rs_n) {
   constexpr int N = Pack<T>::N;
   __shared__ int s_err;
   __shared__ SComm S;
@@ -436,6 +441,14 @@ __global__ void __launch_bounds__(kThreads, 2)
   MCRDL_TRACE_AT(c, bid, kTraceSlots - 1);
 }
 
+template <typename T, int OP, bool VEC, bool TMA>
+__global__ void __launch_bounds__(kThreads, 2) k_ar_pipe(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp, int gs,
+              int64_t chp, uint32_t sig, T* rs_out = nullptr, int64_t rs_n = 0) {
+  const uint32_t epoch = epoch_enter(c);
+  ar_pipe_body<T, OP, VEC, TMA>(c, in, out, n, sp, segb, gp, gs, chp, epoch, sig, rs_out, rs_n);
+  epoch_exit(c, epoch);
+}
+
 // ------------------------------------- warp-specialized two-shot (K2, v3)
 // Same three roles as k_ar_pipe, but inside EVERY CTA as warp groups
 // (senders | reducers | gatherers) synchronised with named barriers, one
@@ -464,8 +477,7 @@ __device__ __forceinline__ void push_packs_g(const T* in, int64_t n, int64_t g0,
 }
 
 template <typename T, int OP, bool VEC>
-__global__ void __launch_bounds__(kThreads, 2)
-    k_ar_ws(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int64_t chp,
+__device__ __forceinline__ void ar_ws_body(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int64_t chp,
             uint32_t epoch, uint32_t sig) {
   constexpr int N = Pack<T>::N;
   constexpr int WS = 6, WR = 6;
@@ -605,6 +617,14 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+template <typename T, int OP, bool VEC>
+__global__ void __launch_bounds__(kThreads, 2) k_ar_ws(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int64_t chp,
+            uint32_t sig) {
+  const uint32_t epoch = epoch_enter(c);
+  ar_ws_body<T, OP, VEC>(c, in, out, n, sp, segb, chp, epoch, sig);
+  epoch_exit(c, epoch);
+}
+
 // ----------------------------------------------------------- NVLS (switch)
 // All-reduce through the NVSwitch multicast object (sum, f32 / bf16):
 //   copiers   [0, gp)     my input, chunk r of share s of EVERY segment ->
@@ -640,8 +660,7 @@ __device__ __forceinline__ void mm_st(void* mc, const uint4& v) {
 }
 
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(kThreads, 2)
-    k_ar_nvls(DevComm c, uint8_t* uc, uint8_t* mc, const T* in, T* out, int64_t n, int64_t sp, int gp,
+__device__ __forceinline__ void ar_nvls_body(DevComm c, uint8_t* uc, uint8_t* mc, const T* in, T* out, int64_t n, int64_t sp, int gp,
               int64_t chp, uint32_t epoch, uint32_t sig) {
   constexpr int N = Pack<T>::N;
   __shared__ int s_err;
@@ -737,6 +756,14 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kThreads, 2) k_ar_nvls(DevComm c, uint8_t* uc, uint8_t* mc, int64_t nv_half, const T* in, T* out, int64_t n,
+              int64_t sp, int gp, int64_t chp, uint32_t sig) {
+  const uint32_t epoch = epoch_enter(c);
+  ar_nvls_body<T, VEC>(c, uc + int64_t(epoch & 1) * nv_half, mc + int64_t(epoch & 1) * nv_half, in, out, n, sp, gp, chp, epoch, sig);
+  epoch_exit(c, epoch);
+}
+
 // ------------------------------------------------------------- fused (K9)
 // Members laid out back to back in a virtual packed buffer (element offsets
 // d_off[m], 16-byte aligned). One-shot protocol over the packed index space:
@@ -745,8 +772,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 // launch (reference: np.concatenate + all_reduce + _scatter_back,
 // middleware.py:316-341).
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads)
-    k_ar_fused(DevComm c, const T* const* in_ptrs, T* const* out_ptrs, const int64_t* counts,
+__device__ __forceinline__ void ar_fused_body(DevComm c, const T* const* in_ptrs, T* const* out_ptrs, const int64_t* counts,
                const int64_t* offs, int nmem, int64_t total, int64_t slot_bytes, uint32_t epoch,
                uint32_t sig) {
   constexpr int N = Pack<T>::N;
@@ -825,6 +851,14 @@ __global__ void __launch_bounds__(kThreads)
       else store_pack<T, false>(dst, li, cnt, acc.to_raw());
     }
   }
+}
+
+template <typename T, int OP>
+__global__ void __launch_bounds__(kThreads) k_ar_fused(DevComm c, const T* const* in_ptrs, T* const* out_ptrs, const int64_t* counts,
+               const int64_t* offs, int nmem, int64_t total, int64_t slot_bytes, uint32_t sig) {
+  const uint32_t epoch = epoch_enter(c);
+  ar_fused_body<T, OP>(c, in_ptrs, out_ptrs, counts, offs, nmem, total, slot_bytes, epoch, sig);
+  epoch_exit(c, epoch);
 }
 
 // Local copy used for world == 1 (the p = 1 floor: out[:] = in).
@@ -926,15 +960,14 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
   int sub = 0;
   do {
     const int64_t m = (n - done < chunk_elems) ? (n - done) : chunk_elems;
-    uint32_t epoch;
-    mcrdl_status_t st = begin_op(c, stream, &epoch);
+    mcrdl_status_t st = begin_op(c, stream);
     if (st != MCRDL_OK) return st;
     const uint32_t sig = op_sig(kKindAllReduce, dt, OP, sub, uint64_t(m), seq);
     const T* ip = in + done;
     T* op = out + done;
     const int64_t npk = (m + N - 1) / N;
     if (algo == MCRDL_ALGO_ONE_SHOT && m * int64_t(sizeof(T)) <= ll_max_bytes()) {
-      st = launch_ar_ll<T, OP>(c, ip, op, m, epoch, sig, stream);
+      st = launch_ar_ll<T, OP>(c, ip, op, m, sig, stream);
       if (st != MCRDL_OK) return st;
       done += m;
       ++sub;
@@ -944,9 +977,9 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
       const int64_t slot = (npk * 16 + 255) / 256 * 256;
       const int G = grid_for(npk, c->num_sms, 64);
       if (vec)
-        k_ar_oneshot<T, OP, true><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, slot, epoch, sig);
+        k_ar_oneshot<T, OP, true><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, slot, sig);
       else
-        k_ar_oneshot<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, slot, epoch, sig);
+        k_ar_oneshot<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, slot, sig);
     } else {
       const int64_t sp = (npk + world - 1) / world;
       const int64_t segb = (sp * 16 + 255) / 256 * 256;
@@ -966,15 +999,16 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
       bool launched = false;
       if constexpr (kNvlsType && OP == MCRDL_SUM) {
         if (algo == MCRDL_ALGO_NVLS) {
-          const int64_t hoff = int64_t(epoch & 1) * int64_t(c->nvls.bytes / 2);
-          uint8_t* uc = reinterpret_cast<uint8_t*>(c->nvls.uc_ptr) + hoff;
-          uint8_t* mc = reinterpret_cast<uint8_t*>(c->nvls.mc_ptr) + hoff;
+          // the kernel picks the multicast half by its device epoch's parity
+          const int64_t nv_half = int64_t(c->nvls.bytes / 2);
+          uint8_t* uc = reinterpret_cast<uint8_t*>(c->nvls.uc_ptr);
+          uint8_t* mc = reinterpret_cast<uint8_t*>(c->nvls.mc_ptr);
           if (vec)
-            k_ar_nvls<T, true><<<G, kThreads, 0, stream>>>(c->dc, uc, mc, ip, op, m, sp, int(gp), chp,
-                                                           epoch, sig);
+            k_ar_nvls<T, true><<<G, kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, ip, op, m, sp,
+                                                           int(gp), chp, sig);
           else
-            k_ar_nvls<T, false><<<G, kThreads, 0, stream>>>(c->dc, uc, mc, ip, op, m, sp, int(gp),
-                                                            chp, epoch, sig);
+            k_ar_nvls<T, false><<<G, kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, ip, op, m, sp,
+                                                            int(gp), chp, sig);
           launched = true;
         }
       }
@@ -997,10 +1031,10 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
         if (ws_kernel == 1) {
           if (vec)
             k_ar_ws<T, OP, true><<<int(gw), kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, chpw,
-                                                                   epoch, sig);
+                                                                   sig);
           else
             k_ar_ws<T, OP, false><<<int(gw), kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, chpw,
-                                                                    epoch, sig);
+                                                                    sig);
         } else if (vec && (tma_on == 2 || (tma_on == 1 && big))) {
           const int gs = int(std::min<int64_t>(gp, tma_ctas));
           int64_t gpt = gp;
@@ -1013,13 +1047,13 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
           int64_t chpt = (sharet + 3999) / 4000;
           if (chpt < chunk_kb * 64) chpt = chunk_kb * 64;
           k_ar_pipe<T, OP, true, true><<<int(gs + 2 * gpt), kThreads, 0, stream>>>(
-              c->dc, ip, op, m, sp, segb, int(gpt), gs, chpt, epoch, sig);
+              c->dc, ip, op, m, sp, segb, int(gpt), gs, chpt, sig);
         } else if (vec) {
           k_ar_pipe<T, OP, true, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb,
-                                                                    int(gp), int(gp), chp, epoch, sig);
+                                                                    int(gp), int(gp), chp, sig);
         } else {
           k_ar_pipe<T, OP, false, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb,
-                                                                     int(gp), int(gp), chp, epoch, sig);
+                                                                     int(gp), int(gp), chp, sig);
         }
       }
     }
@@ -1060,8 +1094,7 @@ static mcrdl_status_t rs_typed(mcrdl_comm* c, const T* in, T* out, int64_t m, ui
       2 * int64_t(world) * ((segbytes + 255) / 256 * 256) > c->dc.half_bytes)
     return set_error(MCRDL_ERR_UNSUPPORTED, "reduce_scatter kernel needs aligned 16-byte segments "
                                             "within one workspace half");
-  uint32_t epoch;
-  mcrdl_status_t st = begin_op(c, stream, &epoch);
+  mcrdl_status_t st = begin_op(c, stream);
   if (st != MCRDL_OK) return st;
   const uint32_t sig = op_sig(kKindReduceScatter, dt, OP, -1, uint64_t(m), seq);
   const int64_t sp = segbytes / 16;
@@ -1071,7 +1104,7 @@ static mcrdl_status_t rs_typed(mcrdl_comm* c, const T* in, T* out, int64_t m, ui
   int64_t chp = ((sp + gp - 1) / gp + 3999) / 4000;
   if (chp < 16384) chp = 16384;
   k_ar_pipe<T, OP, true, false><<<int(3 * gp), kThreads, 0, stream>>>(
-      c->dc, in, out, int64_t(world) * m, sp, segb, int(gp), int(gp), chp, epoch, sig, out, m);
+      c->dc, in, out, int64_t(world) * m, sp, segb, int(gp), int(gp), chp, sig, out, m);
   count_launch();
   MCRDL_CUDA_CHECK(cudaGetLastError());
   return MCRDL_OK;
@@ -1096,8 +1129,7 @@ static mcrdl_status_t fused_typed(mcrdl_comm* c, const void* const* in_ptrs, voi
                                   const int64_t* counts, const int64_t* offs, int nmem,
                                   int64_t total, uint64_t seq, int dt, cudaStream_t stream) {
   constexpr int N = Pack<T>::N;
-  uint32_t epoch;
-  mcrdl_status_t st = begin_op(c, stream, &epoch);
+  mcrdl_status_t st = begin_op(c, stream);
   if (st != MCRDL_OK) return st;
   const int64_t npk = (total + N - 1) / N;
   const int64_t slot = (npk * 16 + 255) / 256 * 256;
@@ -1108,7 +1140,7 @@ static mcrdl_status_t fused_typed(mcrdl_comm* c, const void* const* in_ptrs, voi
   const int G = grid_for(npk, c->num_sms, 64);
   k_ar_fused<T, OP><<<G, kThreads, 0, stream>>>(
       c->dc, reinterpret_cast<const T* const*>(in_ptrs), reinterpret_cast<T* const*>(out_ptrs), counts,
-      offs, nmem, total, slot, epoch, sig);
+      offs, nmem, total, slot, sig);
   count_launch();
   MCRDL_CUDA_CHECK(cudaGetLastError());
   return MCRDL_OK;

@@ -447,7 +447,7 @@ static void teardown_nvls(mcrdl_comm* c) {
   nv = Nvls{};
 }
 
-mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, uint32_t* epoch) {
+mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream) {
   if (comm == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   if (comm->sticky != MCRDL_OK)
     return set_error(comm->sticky, "communicator poisoned by an earlier device error (%s)",
@@ -458,14 +458,19 @@ mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, uint32_t* epoch) 
                      mcrdl_status_kind(comm->sticky));
   }
   if (comm->have_last && comm->last_stream != stream) {
-    MCRDL_CUDA_CHECK(cudaEventRecord(comm->order_ev, comm->last_stream));
-    MCRDL_CUDA_CHECK(cudaStreamWaitEvent(stream, comm->order_ev, 0));
+    // A stream being captured into a CUDA graph cannot wait on work outside
+    // the capture; capture starts from a synchronized device
+    // (torch.cuda.graph does this), and replays are ordered by the caller
+    // like any other op of the communicator.
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    MCRDL_CUDA_CHECK(cudaStreamIsCapturing(stream, &cs));
+    if (cs == cudaStreamCaptureStatusNone) {
+      MCRDL_CUDA_CHECK(cudaEventRecord(comm->order_ev, comm->last_stream));
+      MCRDL_CUDA_CHECK(cudaStreamWaitEvent(stream, comm->order_ev, 0));
+    }
   }
   comm->last_stream = stream;
   comm->have_last = true;
-  comm->epoch += 1;
-  if (comm->epoch == 0) comm->epoch = 1;
-  *epoch = comm->epoch;
   return MCRDL_OK;
 }
 
@@ -581,6 +586,7 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   c->dc.err = c->err_dev;
   c->dc.timeout_ns = c->timeout_ns;
   c->dc.half_bytes = int64_t(workspace_bytes / 2);
+  c->dc.self = reinterpret_cast<Pad*>(c->base.ptr[rank]);
   for (int q = 0; q < world; ++q) {
     c->dc.pad[q] = reinterpret_cast<Pad*>(c->base.ptr[q]);
     c->dc.ws[q] = reinterpret_cast<uint8_t*>(c->base.ptr[q]) + kPadBytes;

@@ -35,6 +35,12 @@ struct Pad {
   uint64_t ack[2][kMaxBlocks][kMaxRanks];    // slot consumed (multi-round)
   uint64_t abort_word[2][2];                 // [par] = {epoch, code}
   uint64_t poison;                           // any rank's error code, never cleared
+  // Local-only words (never written by peers): the device-resident op epoch
+  // (epoch of the last completed launch) and the exit counter of the running
+  // launch. Keeping the epoch on the device makes every launch replayable
+  // from a CUDA graph: no host-baked argument changes between ops.
+  uint32_t dev_epoch;
+  uint32_t done_ctas;
 };
 // Region layout: [flag pad | LL area | workspace]. The LL area is written
 // only by LL kernels (ll.cu), so a stale LL line always carries an older
@@ -52,6 +58,7 @@ static_assert(kLLOffset + 2 * kLLParityBytes <= kPadBytes, "LL area too large");
 struct DevComm {
   uint8_t* ws[kMaxRanks];  // rank r's workspace, mapped in this address space
   Pad* pad[kMaxRanks];     // rank r's signal pad
+  Pad* self;               // == pad[rank] (no runtime-indexed param access)
   int* err;                // host-mapped latched error word
   uint64_t* trace;         // host-mapped timeline (trace builds only), else null
   uint64_t timeout_ns;
@@ -131,6 +138,34 @@ __device__ __forceinline__ void stage_comm(const DevComm& c, SComm& s) {
     for (int r = 0; r < kMaxRanks; ++r) {
       s.ws[r] = c.ws[r];
       s.pad[r] = c.pad[r];
+    }
+  }
+}
+
+// Device-resident epoch. Every CTA of a launch reads the local pad's
+// dev_epoch at entry (the launch's epoch = last + 1, skipping 0); the last CTA
+// to leave stores it back. The store happens only after all gridDim.x CTAs
+// have arrived at the exit counter, i.e. after every CTA has read the old
+// value. Launches of one comm never overlap (stream-ordered; begin_op chains
+// streams), so launch k+1 always sees launch k's store.
+__device__ __forceinline__ uint32_t epoch_enter(const DevComm& c) {
+  __shared__ uint32_t s_epoch;
+  if (threadIdx.x == 0) {
+    const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(&c.self->dev_epoch) + 1u;
+    s_epoch = e == 0u ? 1u : e;
+  }
+  __syncthreads();
+  return s_epoch;
+}
+__device__ __forceinline__ void epoch_exit(const DevComm& c, uint32_t epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t prev = atomicAdd(&c.self->done_ctas, 1u);
+    if (prev == gridDim.x - 1) {
+      *reinterpret_cast<volatile uint32_t*>(&c.self->done_ctas) = 0u;
+      *reinterpret_cast<volatile uint32_t*>(&c.self->dev_epoch) = epoch;
+      __threadfence();
     }
   }
 }

@@ -141,7 +141,7 @@ __device__ __forceinline__ void geo_round(PeerGeo& G, const int64_t* bytes, int 
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a, uint32_t epoch) {
+__device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch) {
   __shared__ const uint8_t* s_sp[kMaxRanks];
   __shared__ uint8_t* s_rp[kMaxRanks];
   __shared__ int64_t s_sb[kMaxRanks];
@@ -273,6 +273,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a, ui
   }
 }
 
+__global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a) {
+  const uint32_t epoch = epoch_enter(c);
+  exchange_body(c, a, epoch);
+  epoch_exit(c, epoch);
+}
+
 mcrdl_status_t launch_local_copy(void* dst, const void* src, int64_t nbytes, int num_sms,
                                  cudaStream_t stream);
 
@@ -285,10 +291,9 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
                        (long long)sp.sbytes[0], (long long)sp.rbytes[0]);
     return launch_local_copy(sp.rptr[0], sp.sptr[0], sp.sbytes[0], c->num_sms, stream);
   }
-  uint32_t epoch;
-  mcrdl_status_t st = begin_op(c, stream, &epoch);
+  mcrdl_status_t st = begin_op(c, stream);
   if (st != MCRDL_OK) return st;
-  if (try_exchange_ll(c, sp, epoch, stream, &st)) return st;
+  if (try_exchange_ll(c, sp, stream, &st)) return st;
   XArgs a;
   memset(&a, 0, sizeof(a));
   for (int r = 0; r < c->world; ++r) {
@@ -324,7 +329,7 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
     }
   }
   a.gp = int(g);
-  k_exchange<<<int(2 * g), kThreads, 0, stream>>>(c->dc, a, epoch);
+  k_exchange<<<int(2 * g), kThreads, 0, stream>>>(c->dc, a);
   count_launch();
   MCRDL_CUDA_CHECK(cudaGetLastError());
   return MCRDL_OK;

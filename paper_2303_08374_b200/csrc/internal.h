@@ -54,7 +54,6 @@ struct mcrdl_comm {
   mcrdl::Nvls nvls;
   int* err_host = nullptr;            // cudaHostAllocMapped
   int* err_dev = nullptr;
-  uint32_t epoch = 0;                 // launches so far (flag epoch)
   uint64_t timeout_ns = 30ull * 1000000000ull;
   uint64_t ws_bytes = 0;
   mcrdl::DevComm dc{};
@@ -82,9 +81,10 @@ void count_launch();
                                 cudaGetErrorString(e_), __FILE__, __LINE__);          \
   } while (0)
 
-// Validates the comm, orders `stream` after the comm's previous op and
-// returns the next epoch (>= 1).
-mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, uint32_t* epoch);
+// Validates the comm and orders `stream` after the comm's previous op. The
+// op epoch itself lives on the device (Pad::dev_epoch, common.cuh), so a
+// launch carries no per-op host state and can be replayed from a CUDA graph.
+mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream);
 
 inline int64_t env_int(const char* name, int64_t dflt) {
   const char* e = getenv(name);
@@ -147,10 +147,10 @@ mcrdl_status_t launch_exchange(mcrdl_comm* comm, const ExchangeSpec& spec, int64
 // LL protocol (ll.cu) for small messages.
 constexpr int64_t kLLMaxPairBytes = 64 << 10;      // exchange: every pair <= this
 constexpr int64_t kLLMaxAllReduceBytes = 64 << 10; // all_reduce one-shot message <= this
-bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, uint32_t epoch, cudaStream_t stream,
+bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, cudaStream_t stream,
                      mcrdl_status_t* st);
 template <typename T, int OP>
-mcrdl_status_t launch_ar_ll(mcrdl_comm* c, const T* in, T* out, int64_t n, uint32_t epoch,
+mcrdl_status_t launch_ar_ll(mcrdl_comm* c, const T* in, T* out, int64_t n,
                             uint32_t sig, cudaStream_t stream);
 
 }  // namespace mcrdl

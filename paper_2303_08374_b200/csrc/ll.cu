@@ -28,8 +28,7 @@ namespace mcrdl {
 // rank) straight into `out`, loading all peers' lines of a unit before
 // checking any. Bit-identical to the oracle.
 template <typename T, int OP>
-__global__ void __launch_bounds__(kLLThreads)
-    k_ar_ll(DevComm c, const T* in, T* out, int64_t n, uint32_t epoch, uint32_t sig) {
+__device__ __forceinline__ void ar_ll_body(DevComm c, const T* in, T* out, int64_t n, uint32_t epoch, uint32_t sig) {
   constexpr int E = 8 / int(sizeof(T));  // elements per 8-byte unit
   using A = typename AccT<T>::type;
   __shared__ SComm S;
@@ -100,21 +99,28 @@ __global__ void __launch_bounds__(kLLThreads)
 }
 
 template <typename T, int OP>
-mcrdl_status_t launch_ar_ll(mcrdl_comm* c, const T* in, T* out, int64_t n, uint32_t epoch,
+__global__ void __launch_bounds__(kLLThreads) k_ar_ll(DevComm c, const T* in, T* out, int64_t n, uint32_t sig) {
+  const uint32_t epoch = epoch_enter(c);
+  ar_ll_body<T, OP>(c, in, out, n, epoch, sig);
+  epoch_exit(c, epoch);
+}
+
+template <typename T, int OP>
+mcrdl_status_t launch_ar_ll(mcrdl_comm* c, const T* in, T* out, int64_t n,
                             uint32_t sig, cudaStream_t stream) {
   const int64_t nu = (n * int64_t(sizeof(T)) + 7) / 8;
   if (nu * 8 > kLLMaxPayload)
     return set_error(MCRDL_ERR_INTERNAL, "LL all_reduce above the LL slot size");
   int64_t g = (nu + kLLThreads - 1) / kLLThreads;
   g = std::max<int64_t>(1, std::min<int64_t>(g, 32));
-  k_ar_ll<T, OP><<<int(g), kLLThreads, 0, stream>>>(c->dc, in, out, n, epoch, sig);
+  k_ar_ll<T, OP><<<int(g), kLLThreads, 0, stream>>>(c->dc, in, out, n, sig);
   count_launch();
   MCRDL_CUDA_CHECK(cudaGetLastError());
   return MCRDL_OK;
 }
 
 #define INST_AR_LL(T, OP)                                                                       \
-  template mcrdl_status_t launch_ar_ll<T, OP>(mcrdl_comm*, const T*, T*, int64_t, uint32_t,     \
+  template mcrdl_status_t launch_ar_ll<T, OP>(mcrdl_comm*, const T*, T*, int64_t,     \
                                               uint32_t, cudaStream_t);
 #define INST_AR_LL_T(T) INST_AR_LL(T, 0) INST_AR_LL(T, 1) INST_AR_LL(T, 2) INST_AR_LL(T, 3)
 INST_AR_LL_T(float)
@@ -127,7 +133,7 @@ INST_AR_LL_T(__nv_bfloat16)
 // -------------------------------------------------------------- exchange
 // All of this rank's pairs are LL pairs: G CTAs, CTA b moves units
 // [nu*b/G, nu*(b+1)/G) of every pair; CTA 0 also writes / checks headers.
-__global__ void __launch_bounds__(kLLThreads) k_exchange_ll(DevComm c, LLArgs a, uint32_t epoch) {
+__device__ __forceinline__ void exchange_ll_body(DevComm c, LLArgs a, uint32_t epoch) {
   __shared__ SComm S;
   __shared__ int s_err;
   const int par = epoch & 1, rank = c.rank, world = c.world;
@@ -160,10 +166,16 @@ __global__ void __launch_bounds__(kLLThreads) k_exchange_ll(DevComm c, LLArgs a,
   }
 }
 
+__global__ void __launch_bounds__(kLLThreads) k_exchange_ll(DevComm c, LLArgs a) {
+  const uint32_t epoch = epoch_enter(c);
+  exchange_ll_body(c, a, epoch);
+  epoch_exit(c, epoch);
+}
+
 // Returns true when every pair of this rank is an LL pair (the LL kernel
 // then takes the whole op; peers may still run k_exchange for their bulk
 // pairs with other ranks).
-bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, uint32_t epoch, cudaStream_t stream,
+bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, cudaStream_t stream,
                      mcrdl_status_t* st) {
   int64_t mx = 0;
   for (int r = 0; r < c->world; ++r) {
@@ -183,7 +195,7 @@ bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, uint32_t epoch, cuda
   int64_t g = (mx / 8 + kLLThreads * 2 - 1) / (kLLThreads * 2);
   g = std::max<int64_t>(g, (sp.sbytes[c->rank] + (256 << 10) - 1) >> 18);
   g = std::max<int64_t>(1, std::min<int64_t>(g, 16));
-  k_exchange_ll<<<int(g), kLLThreads, 0, stream>>>(c->dc, a, epoch);
+  k_exchange_ll<<<int(g), kLLThreads, 0, stream>>>(c->dc, a);
   count_launch();
   cudaError_t e = cudaGetLastError();
   *st = e == cudaSuccess ? MCRDL_OK

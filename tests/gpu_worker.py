@@ -402,6 +402,73 @@ def sc_order_mismatch(cx: Ctx):
         cx.failures.append(f"order_mismatch: expected OrderMismatch, got {raised!r}")
 
 
+def sc_graphs(cx: Ctx):
+    """Collectives captured into one CUDA graph and replayed with fresh inputs,
+    eager ops interleaved between replays. Works because the op epoch lives
+    on the device (common.cuh epoch_enter/epoch_exit): a replayed launch has
+    no host-baked per-op state. Covers the LL, one-shot, two-shot (and NVLS
+    when present) all_reduce kernels and the exchange kernel."""
+    p, r, dev = cx.p, cx.r, cx.dev
+    inst = cx.rt._instance(cx.b)
+    sizes = {"ll": 1000, "one_shot": 300_003, "two_shot": (24 << 20) // 4 + 3}
+    xs = {k: torch.empty(n, dtype=torch.float32, device=dev) for k, n in sizes.items()}
+    outs = {k: torch.empty_like(v) for k, v in xs.items()}
+    nv = bool(inst.comm.caps.nvls_supported) and p > 1
+    nv_x = torch.empty(1 << 18, dtype=torch.float32, device=dev)
+    m = 4099
+    a_in = torch.empty(p * m, dtype=torch.int64, device=dev)
+    a_out = torch.empty_like(a_in)
+
+    def run_ops():
+        for k in xs:
+            inst.policy = AlgorithmPolicy({CommOpKind.all_reduce: k if k != "ll" else "auto"})
+            cx.rt.post(CommRequest(CommOpKind.all_reduce, input=Buffer(xs[k]),
+                                   output=Buffer(outs[k]), op=ReduceOp.sum, backend=cx.b))
+        if nv:
+            inst.policy = AlgorithmPolicy({CommOpKind.all_reduce: "nvls"})
+            cx.rt.all_reduce(cx.b, Buffer(nv_x))
+        inst.policy = AlgorithmPolicy()
+        cx.rt.all_to_all_single(cx.b, Buffer(a_out), Buffer(a_in))
+
+    def fill(it):
+        ins = {k: [values(DType.f32, n, "graph", k, it, q) for q in range(p)]
+               for k, n in sizes.items()}
+        nvi = [values(DType.f32, nv_x.numel(), "graph-nv", it, q) for q in range(p)]
+        a = [values(DType.i64, p * m, "graph-a2a", it, q) for q in range(p)]
+        for k in xs:
+            xs[k].copy_(torch.from_numpy(ins[k][r]))
+        nv_x.copy_(torch.from_numpy(nvi[r]))
+        a_in.copy_(torch.from_numpy(a[r]))
+        return ins, nvi, a
+
+    def verify(tag, ins, nvi, a):
+        for k in xs:
+            cx.check(f"graph/{tag}/{k}", from_dev(outs[k], DType.f32), seqref.fold(ins[k], "sum"))
+        if nv:
+            cx.check(f"graph/{tag}/nvls", from_dev(nv_x, DType.f32), seqref.fold(nvi, "sum"),
+                     float_reduction=True, rtol=1e-5)
+        cx.check(f"graph/{tag}/a2a", from_dev(a_out, DType.i64), seqref.all_to_all_single(a)[r])
+
+    state = fill(0)
+    run_ops()  # eager warm-up outside the capture
+    torch.cuda.synchronize()
+    verify("eager", *state)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run_ops()
+    for it in range(1, 5):
+        state = fill(it)
+        g.replay()
+        # an eager op between replays keeps the device epoch in step
+        e = [values(DType.i32, 777, "graph-eager", it, q) for q in range(p)]
+        t = to_dev(e[r], DType.i32, dev)
+        cx.rt.all_reduce(cx.b, Buffer(t))
+        torch.cuda.synchronize()
+        verify(f"replay{it}", *state)
+        cx.check(f"graph/eager{it}", from_dev(t, DType.i32), seqref.fold(e, "sum"))
+    del g
+
+
 def sc_smoke(cx: Ctx):
     """One small invocation of each hot-path family (smoke())."""
     p, r = cx.p, cx.r
@@ -529,6 +596,7 @@ SCENARIOS = {
     "reduce_family": sc_reduce_family,
     "host_buffers": sc_host_buffers,
     "async_fusion": sc_async_and_fusion,
+    "graphs": sc_graphs,
     "order_mismatch": sc_order_mismatch,
 }
 
