@@ -187,6 +187,18 @@ mcrdl_status_t mcrdl_bcast(mcrdl_comm* comm, void* buf, uint64_t count, mcrdl_dt
                            int root, mcrdl_algo_t algo, uint64_t seq, void* stream);
 /* 0-byte collective used as a barrier by the tuner (tuner.py:151-159). */
 mcrdl_status_t mcrdl_barrier(mcrdl_comm* comm, uint64_t seq, void* stream);
+/* Point-to-point (Runtime.send / Runtime.recv, runtime.py:498-508, executed by
+ * BackendInstance.execute, runtime.py:244-262). Only the two endpoints take
+ * part; no collective sequence number is consumed. Messages are matched in
+ * post order per (sender, receiver) pair. send is eager up to 256 queued
+ * messages and the per-sender mailbox (MCRDL_P2P_BYTES, default 32 MiB) and
+ * streams larger messages through it (the matching recv must then be in
+ * flight: post it first, on another stream). Sends, receives and collectives
+ * are ordered only within their own kind, so a recv may overlap a send. A byte-count
+ * difference latches MCRDL_ERR_LENGTH_MISMATCH on the receiver (runtime.py:
+ * 256-260). peer == own rank is allowed. */
+mcrdl_status_t mcrdl_send(mcrdl_comm* comm, const void* buf, uint64_t bytes, int peer, void* stream);
+mcrdl_status_t mcrdl_recv(mcrdl_comm* comm, void* buf, uint64_t bytes, int peer, void* stream);
 
 /* ----------------------------------------------------------------- fusion */
 /* Tensor fusion (middleware.py:222-359). Segment tables are device arrays of

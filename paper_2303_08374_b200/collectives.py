@@ -16,6 +16,7 @@ all_gather(v)      auto, direct_write
 gather(v)          auto, direct_write
 scatter(v)         auto, direct_write
 all_to_all*        auto, direct_write
+send / recv        direct                            (per-pair mailbox ring)
 =================  ======================================================
 
 "auto" = per message size from the runtime's tuning table, else the
@@ -50,13 +51,12 @@ ALGORITHMS: Dict[CommOpKind, Tuple[str, ...]] = {
     CommOpKind.all_to_all_single: _MOVE,
     CommOpKind.all_to_all: _MOVE,
     CommOpKind.all_to_allv: _MOVE,
-    CommOpKind.send: (),
-    CommOpKind.recv: (),
+    CommOpKind.send: ("direct",),
+    CommOpKind.recv: ("direct",),
 }
 
-# Point-to-point send/recv are not collective over the NVLink communicator
-# (every kernel is a whole-world exchange); they stay out of scope.
-UNSUPPORTED_KINDS = frozenset({CommOpKind.send, CommOpKind.recv})
+# Every kind has a native path (send/recv: csrc/p2p.cu).
+UNSUPPORTED_KINDS: frozenset = frozenset()
 
 DEFAULT_ALGORITHMS: Dict[CommOpKind, str] = {
     k: (v[0] if v else "unsupported") for k, v in ALGORITHMS.items()
@@ -73,7 +73,7 @@ ALIASES: Dict[str, str] = {
 }
 
 # Native algorithm codes (include/mcrdl_nvl.h mcrdl_algo_t).
-ALGO_CODES = {"auto": 0, "one_shot": 1, "two_shot": 2, "nvls": 3, "direct_write": 4}
+ALGO_CODES = {"auto": 0, "one_shot": 1, "two_shot": 2, "nvls": 3, "direct_write": 4, "direct": 0}
 
 
 def canonical(kind: CommOpKind, name: str) -> str:

@@ -246,8 +246,9 @@ __device__ __forceinline__ void tma_drain() {
 }
 
 template <typename T, int OP, bool VEC, bool TMA>
-__device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp, int gs,
-              int64_t chp, uint32_t epoch, uint32_t sig, T* rs_out, int64_t rs_n) {
+__device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int64_t n, int64_t sp,
+                                             int64_t segb, int gp, int gs, int64_t chp, int ag_pull,
+                                             uint32_t epoch, uint32_t sig, T* rs_out, int64_t rs_n) {
   constexpr int N = Pack<T>::N;
   __shared__ int s_err;
   __shared__ SComm S;
@@ -385,9 +386,13 @@ __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int
             store_pack<T, VEC>(rs_out, i, rs_n, res);
             continue;
           }
-          for (int k = 1; k < world; ++k) {
-            const int q = (rank + k) % world;
-            st16(S.ws[q] + hoff + ag + int64_t(rank) * segb + i * 16, res);
+          if (ag_pull) {  // peers pull it from my workspace
+            st16(S.ws[rank] + hoff + ag + int64_t(rank) * segb + i * 16, res);
+          } else {
+            for (int k = 1; k < world; ++k) {
+              const int q = (rank + k) % world;
+              st16(S.ws[q] + hoff + ag + int64_t(rank) * segb + i * 16, res);
+            }
           }
           store_pack<T, VEC>(out, int64_t(rank) * sp + i, n, res);
         }
@@ -425,8 +430,20 @@ __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int
       const int64_t lo = int64_t(r) * chp;
       if (lo >= len) continue;
       const int64_t hi = min(len, lo + chp);
-      const uint8_t* src = ws + ag + int64_t(q) * segb;
       int64_t i = rb + lo + tid;
+      if (ag_pull) {  // remote reads of rank q's reduced segment: 8 packs in flight
+        const uint8_t* src = S.ws[q] + hoff + ag + int64_t(q) * segb;
+        for (; i + 7 * nt < rb + hi; i += 8 * nt) {
+          uint4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = ld16_cg(src + (i + u * nt) * 16);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) store_pack<T, VEC>(out, int64_t(q) * sp + i + u * nt, n, v[u]);
+        }
+        for (; i < rb + hi; i += nt) store_pack<T, VEC>(out, int64_t(q) * sp + i, n, ld16_cg(src + i * 16));
+        continue;
+      }
+      const uint8_t* src = ws + ag + int64_t(q) * segb;
       for (; i + 3 * nt < rb + hi; i += 4 * nt) {
         uint4 v[4];
 #pragma unroll
@@ -442,10 +459,12 @@ __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int
 }
 
 template <typename T, int OP, bool VEC, bool TMA>
-__global__ void __launch_bounds__(kThreads, 2) k_ar_pipe(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp, int gs,
-              int64_t chp, uint32_t sig, T* rs_out = nullptr, int64_t rs_n = 0) {
+__global__ void __launch_bounds__(kThreads, 2)
+    k_ar_pipe(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp, int gs,
+              int64_t chp, int ag_pull, uint32_t sig, T* rs_out = nullptr, int64_t rs_n = 0) {
   const uint32_t epoch = epoch_enter(c);
-  ar_pipe_body<T, OP, VEC, TMA>(c, in, out, n, sp, segb, gp, gs, chp, epoch, sig, rs_out, rs_n);
+  ar_pipe_body<T, OP, VEC, TMA>(c, in, out, n, sp, segb, gp, gs, chp, ag_pull, epoch, sig, rs_out,
+                                rs_n);
   epoch_exit(c, epoch);
 }
 
@@ -660,8 +679,9 @@ __device__ __forceinline__ void mm_st(void* mc, const uint4& v) {
 }
 
 template <typename T, bool VEC>
-__device__ __forceinline__ void ar_nvls_body(DevComm c, uint8_t* uc, uint8_t* mc, const T* in, T* out, int64_t n, int64_t sp, int gp,
-              int64_t chp, uint32_t epoch, uint32_t sig) {
+__device__ __forceinline__ void ar_nvls_body(DevComm c, uint8_t* uc, uint8_t* mc, const T* in,
+                                             T* out, int64_t n, int64_t sp, int gp, int64_t chp,
+                                             int fence, uint32_t epoch, uint32_t sig) {
   constexpr int N = Pack<T>::N;
   __shared__ int s_err;
   __shared__ SComm S;
@@ -716,7 +736,7 @@ __device__ __forceinline__ void ar_nvls_body(DevComm c, uint8_t* uc, uint8_t* mc
         for (int u = 0; u < 4; ++u) mm_st(mc + (base + i + u * nt) * 16, v[u]);
       }
       for (; i < hi; i += nt) mm_st(mc + (base + i) * 16, mm_ld_reduce_sum<T>(mc + (base + i) * 16));
-      __threadfence_system();  // multicast stores complete on every rank before the flag
+      if (fence) __threadfence_system();  // multicast stores complete on every rank before the flag
       __syncthreads();
       if (tid < world) publish(&S.pad[tid]->flag2[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
     }
@@ -757,10 +777,12 @@ __device__ __forceinline__ void ar_nvls_body(DevComm c, uint8_t* uc, uint8_t* mc
 }
 
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(kThreads, 2) k_ar_nvls(DevComm c, uint8_t* uc, uint8_t* mc, int64_t nv_half, const T* in, T* out, int64_t n,
-              int64_t sp, int gp, int64_t chp, uint32_t sig) {
+__global__ void __launch_bounds__(kThreads, 2)
+    k_ar_nvls(DevComm c, uint8_t* uc, uint8_t* mc, int64_t nv_half, const T* in, T* out, int64_t n,
+              int64_t sp, int gp, int64_t chp, int fence, uint32_t sig) {
   const uint32_t epoch = epoch_enter(c);
-  ar_nvls_body<T, VEC>(c, uc + int64_t(epoch & 1) * nv_half, mc + int64_t(epoch & 1) * nv_half, in, out, n, sp, gp, chp, epoch, sig);
+  const int64_t hoff = int64_t(epoch & 1) * nv_half;
+  ar_nvls_body<T, VEC>(c, uc + hoff, mc + hoff, in, out, n, sp, gp, chp, fence, epoch, sig);
   epoch_exit(c, epoch);
 }
 
@@ -1003,12 +1025,13 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
           const int64_t nv_half = int64_t(c->nvls.bytes / 2);
           uint8_t* uc = reinterpret_cast<uint8_t*>(c->nvls.uc_ptr);
           uint8_t* mc = reinterpret_cast<uint8_t*>(c->nvls.mc_ptr);
+          static const int fence = int(env_int("MCRDL_NVLS_FENCE", 1));
           if (vec)
             k_ar_nvls<T, true><<<G, kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, ip, op, m, sp,
-                                                           int(gp), chp, sig);
+                                                           int(gp), chp, fence, sig);
           else
             k_ar_nvls<T, false><<<G, kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, ip, op, m, sp,
-                                                            int(gp), chp, sig);
+                                                            int(gp), chp, fence, sig);
           launched = true;
         }
       }
@@ -1023,6 +1046,8 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
         // MCRDL_AR_KERNEL=1 selects it, 0 the CTA-role kernels below.
         // Measured (tools/ws_ab.sh): p=2 +2%, p=4 -9% at 256 MiB -> default off.
         static const int64_t ws_kernel = env_int("MCRDL_AR_KERNEL", 0);
+        // All-gather half: 1 = peers pull reduced segments, 0 = reducers push.
+        static const int ag_pull = int(env_int("MCRDL_AR_AG_PULL", 0));
         int64_t gw = (sp * 16 + (32 << 10) - 1) / (32 << 10);
         gw = std::max<int64_t>(1, std::min<int64_t>(gw, std::min<int64_t>(2 * c->num_sms, kMaxBlocks)));
         const int64_t sharew = (sp + gw - 1) / gw;
@@ -1047,13 +1072,13 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
           int64_t chpt = (sharet + 3999) / 4000;
           if (chpt < chunk_kb * 64) chpt = chunk_kb * 64;
           k_ar_pipe<T, OP, true, true><<<int(gs + 2 * gpt), kThreads, 0, stream>>>(
-              c->dc, ip, op, m, sp, segb, int(gpt), gs, chpt, sig);
+              c->dc, ip, op, m, sp, segb, int(gpt), gs, chpt, ag_pull, sig);
         } else if (vec) {
-          k_ar_pipe<T, OP, true, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb,
-                                                                    int(gp), int(gp), chp, sig);
+          k_ar_pipe<T, OP, true, false><<<G, kThreads, 0, stream>>>(
+              c->dc, ip, op, m, sp, segb, int(gp), int(gp), chp, ag_pull, sig);
         } else {
-          k_ar_pipe<T, OP, false, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb,
-                                                                     int(gp), int(gp), chp, sig);
+          k_ar_pipe<T, OP, false, false><<<G, kThreads, 0, stream>>>(
+              c->dc, ip, op, m, sp, segb, int(gp), int(gp), chp, ag_pull, sig);
         }
       }
     }
@@ -1103,8 +1128,9 @@ static mcrdl_status_t rs_typed(mcrdl_comm* c, const T* in, T* out, int64_t m, ui
   gp = std::max<int64_t>(1, std::min<int64_t>(gp, 2 * c->num_sms / 3));
   int64_t chp = ((sp + gp - 1) / gp + 3999) / 4000;
   if (chp < 16384) chp = 16384;
-  k_ar_pipe<T, OP, true, false><<<int(3 * gp), kThreads, 0, stream>>>(
-      c->dc, in, out, int64_t(world) * m, sp, segb, int(gp), int(gp), chp, sig, out, m);
+  // senders + reducers only (reduce_scatter has no all-gather role)
+  k_ar_pipe<T, OP, true, false><<<int(2 * gp), kThreads, 0, stream>>>(
+      c->dc, in, out, int64_t(world) * m, sp, segb, int(gp), int(gp), chp, 0, sig, out, m);
   count_launch();
   MCRDL_CUDA_CHECK(cudaGetLastError());
   return MCRDL_OK;

@@ -447,7 +447,7 @@ static void teardown_nvls(mcrdl_comm* c) {
   nv = Nvls{};
 }
 
-mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream) {
+mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, int chain) {
   if (comm == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   if (comm->sticky != MCRDL_OK)
     return set_error(comm->sticky, "communicator poisoned by an earlier device error (%s)",
@@ -457,7 +457,8 @@ mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream) {
     return set_error(comm->sticky, "communicator poisoned by an earlier device error (%s)",
                      mcrdl_status_kind(comm->sticky));
   }
-  if (comm->have_last && comm->last_stream != stream) {
+  auto& ch = comm->chain[chain];
+  if (ch.have && ch.last != stream) {
     // A stream being captured into a CUDA graph cannot wait on work outside
     // the capture; capture starts from a synchronized device
     // (torch.cuda.graph does this), and replays are ordered by the caller
@@ -465,12 +466,12 @@ mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     MCRDL_CUDA_CHECK(cudaStreamIsCapturing(stream, &cs));
     if (cs == cudaStreamCaptureStatusNone) {
-      MCRDL_CUDA_CHECK(cudaEventRecord(comm->order_ev, comm->last_stream));
-      MCRDL_CUDA_CHECK(cudaStreamWaitEvent(stream, comm->order_ev, 0));
+      MCRDL_CUDA_CHECK(cudaEventRecord(ch.ev, ch.last));
+      MCRDL_CUDA_CHECK(cudaStreamWaitEvent(stream, ch.ev, 0));
     }
   }
-  comm->last_stream = stream;
-  comm->have_last = true;
+  ch.last = stream;
+  ch.have = true;
   return MCRDL_OK;
 }
 
@@ -558,7 +559,14 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   if (workspace_bytes == 0) workspace_bytes = uint64_t(1) << 30;
   workspace_bytes = (workspace_bytes + 2 * c->gran - 1) / (2 * c->gran) * (2 * c->gran);
   c->ws_bytes = workspace_bytes;
-  if ((st = alloc_region(c, kPadBytes + workspace_bytes, &c->base)) != MCRDL_OK) return fail(st);
+  // Point-to-point mailboxes after the workspace: one ring per sender
+  // (MCRDL_P2P_BYTES per sender, multiple of 512 KiB, <= 32 MiB; 0 disables).
+  int64_t mbox = int64_t(env_int("MCRDL_P2P_BYTES", int64_t(kP2PSlots) * kP2PChunk));
+  mbox = std::min<int64_t>(mbox, int64_t(kP2PSlots) * kP2PChunk) / kP2PChunk * kP2PChunk;
+  if (mbox < 0) mbox = 0;
+  const uint64_t p2p_bytes = uint64_t(mbox) * uint64_t(world);
+  if ((st = alloc_region(c, kPadBytes + workspace_bytes + p2p_bytes, &c->base)) != MCRDL_OK)
+    return fail(st);
   MCRDL_CUDA_CHECK(cudaMemset(reinterpret_cast<void*>(c->base.ptr[rank]), 0, kPadBytes));
   MCRDL_CUDA_CHECK(cudaDeviceSynchronize());
 
@@ -571,7 +579,7 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
                                  cudaHostAllocMapped | cudaHostAllocPortable));
   *c->err_host = 0;
   MCRDL_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
-  MCRDL_CUDA_CHECK(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
+  for (auto& ch : c->chain) MCRDL_CUDA_CHECK(cudaEventCreateWithFlags(&ch.ev, cudaEventDisableTiming));
 #ifdef MCRDL_TRACE
   {
     const size_t tb = size_t(kMaxBlocks) * kTraceSlots * sizeof(uint64_t);
@@ -586,6 +594,7 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   c->dc.err = c->err_dev;
   c->dc.timeout_ns = c->timeout_ns;
   c->dc.half_bytes = int64_t(workspace_bytes / 2);
+  c->dc.mbox_bytes = mbox;
   c->dc.self = reinterpret_cast<Pad*>(c->base.ptr[rank]);
   for (int q = 0; q < world; ++q) {
     c->dc.pad[q] = reinterpret_cast<Pad*>(c->base.ptr[q]);
@@ -606,7 +615,8 @@ mcrdl_status_t mcrdl_comm_destroy(mcrdl_comm* c) {
   unmap_region(c, c->base);
   teardown_nvls(c);
   if (c->err_host) cudaFreeHost(c->err_host);
-  if (c->order_ev) cudaEventDestroy(c->order_ev);
+  for (auto& ch : c->chain)
+    if (ch.ev) cudaEventDestroy(ch.ev);
   if (c->trace_host) cudaFreeHost(c->trace_host);
   if (c->listen_fd >= 0) close(c->listen_fd);
   delete c;

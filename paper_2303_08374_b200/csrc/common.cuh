@@ -28,6 +28,11 @@ namespace mcrdl {
 constexpr int kMaxRanks = MCRDL_MAX_RANKS;
 constexpr int kMaxBlocks = 512;  // flag slots per parity
 constexpr int kThreads = 512;
+// Point-to-point mailboxes (p2p.cu): every rank owns one ring of kP2PSlots x
+// kP2PChunk bytes per sender; kP2PHdr message headers per sender.
+constexpr int kP2PSlots = 64;
+constexpr int64_t kP2PChunk = 512 << 10;
+constexpr int kP2PHdr = 256;
 
 struct Pad {
   uint64_t flag[2][kMaxBlocks][kMaxRanks];   // data-ready, phase 1
@@ -41,6 +46,15 @@ struct Pad {
   // from a CUDA graph: no host-baked argument changes between ops.
   uint32_t dev_epoch;
   uint32_t done_ctas;
+  // Point-to-point channel (p2p.cu). Written by the peer named in [.]:
+  uint64_t p2p_full[kMaxRanks][kP2PSlots];   // [src][slot] = chunk index + 1 now in the slot
+  uint64_t p2p_free[kMaxRanks][kP2PSlots];   // [dst][slot] = chunk index + 1 dst consumed
+  uint64_t p2p_hdr[kMaxRanks][kP2PHdr][2];   // [src][msg % H] = {msg + 1, bytes}
+  uint64_t p2p_hdr_ack[kMaxRanks];           // [dst] = messages dst has matched
+  // Local-only per-peer stream counters (device-resident: graph-safe).
+  uint64_t p2p_tx_chunks[kMaxRanks], p2p_tx_msgs[kMaxRanks];
+  uint64_t p2p_rx_chunks[kMaxRanks], p2p_rx_msgs[kMaxRanks];
+  uint32_t p2p_done[2];  // exit counters of the running send / recv launch
 };
 // Region layout: [flag pad | LL area | workspace]. The LL area is written
 // only by LL kernels (ll.cu), so a stale LL line always carries an older
@@ -63,6 +77,7 @@ struct DevComm {
   uint64_t* trace;         // host-mapped timeline (trace builds only), else null
   uint64_t timeout_ns;
   int64_t half_bytes;      // bytes per workspace half
+  int64_t mbox_bytes;      // p2p mailbox per sender (at ws + 2 * half_bytes)
   int rank;
   int world;
 };
@@ -219,6 +234,27 @@ static __device__ __noinline__ int wait_flag(const uint64_t* p, const Pad* me, u
       // spinning thread measurably slowed the bandwidth kernels; raise_error
       // mirrors the code into every rank's device-side pad->poison instead)
       (void)err;
+      if (const uint64_t pz = ld_relaxed_sys(&me->poison)) return int(pz);
+      const uint64_t now = globaltimer_ns();
+      if (start == 0) {
+        start = now;
+      } else if (now - start > timeout_ns) {
+        return MCRDL_ERR_TIMEOUT;
+      }
+    }
+  }
+}
+
+// Spin until the monotone counter at `p` reaches `target` (p2p channel);
+// bounded by the timeout and by the poison word like wait_flag.
+static __device__ __noinline__ int wait_geq(const uint64_t* p, const Pad* me, uint64_t timeout_ns,
+                                            uint64_t target) {
+  uint64_t start = 0;
+  int spins = 0;
+  for (;;) {
+    if (ld_acquire_sys(p) >= target) return MCRDL_OK;
+    if (++spins >= 32) {
+      spins = 0;
       if (const uint64_t pz = ld_relaxed_sys(&me->poison)) return int(pz);
       const uint64_t now = globaltimer_ns();
       if (start == 0) {

@@ -58,12 +58,17 @@ struct mcrdl_comm {
   uint64_t ws_bytes = 0;
   mcrdl::DevComm dc{};
   int sticky = MCRDL_OK;              // poisoned after a device error
-  // Every op of a communicator must run in issue order on the device (flag
-  // epochs). Ops may be issued on different streams: when the stream
-  // changes, the new stream waits for the previous one (event, no host sync).
-  cudaEvent_t order_ev = nullptr;
-  cudaStream_t last_stream = nullptr;
-  bool have_last = false;
+  // Ops of one order chain must run in issue order on the device (flag
+  // epochs / p2p stream counters / the shared exit counter). Ops may be
+  // issued on different streams: when the stream changes, the new stream
+  // waits for the previous one (event, no host sync). Chains: collectives,
+  // sends, receives — they use disjoint pad words, so a recv may run
+  // concurrently with a send or a collective on another stream.
+  struct Chain {
+    cudaEvent_t ev = nullptr;
+    cudaStream_t last = nullptr;
+    bool have = false;
+  } chain[3];
   uint64_t* trace_host = nullptr;  // trace builds: kMaxBlocks x kTraceSlots stamps
 };
 
@@ -84,7 +89,8 @@ void count_launch();
 // Validates the comm and orders `stream` after the comm's previous op. The
 // op epoch itself lives on the device (Pad::dev_epoch, common.cuh), so a
 // launch carries no per-op host state and can be replayed from a CUDA graph.
-mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream);
+enum : int { kChainCollective = 0, kChainSend = 1, kChainRecv = 2 };
+mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, int chain = kChainCollective);
 
 inline int64_t env_int(const char* name, int64_t dflt) {
   const char* e = getenv(name);

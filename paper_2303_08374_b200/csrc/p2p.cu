@@ -1,0 +1,209 @@
+// Point-to-point send/recv over NVLink (reference: Runtime.send/recv,
+// runtime.py:498-508, executed by BackendInstance.execute, runtime.py:244-262).
+//
+// Reference semantics restated:
+//  * send is eager: the payload is queued on the transport and the sender
+//    moves on (transport.send, transport.py:175);
+//  * recv blocks for the next payload frame from `peer`; a byte count that
+//    differs from the posted buffer raises LengthMismatch (runtime.py:256-260);
+//  * no header agreement and no collective sequence number: only the two
+//    endpoints take part.
+//
+// Device design. Every rank owns, after its collective workspace, one mailbox
+// per sender: a ring of K = mbox_bytes / 512 KiB chunk slots. A message of B
+// bytes is ceil(B / 512 KiB) chunks numbered on a per-(src, dst) stream that
+// never resets (device-resident counters in the local pad, so no host state
+// changes between messages and launches replay from CUDA graphs):
+//  * sender CTA b moves chunks b, b+G, ...: waits until dst freed the slot
+//    (p2p_free >= g - K + 1), pushes the chunk into dst's mailbox over NVLink,
+//    publishes p2p_full[src][slot] = g + 1 in dst's pad (release);
+//  * receiver CTA b waits p2p_full >= g + 1, copies the slot into the user
+//    buffer, publishes p2p_free[dst][slot] = g + 1 in the sender's pad;
+//  * a per-message header {msg + 1, bytes} (256-deep ring, acked by the
+//    receiver) carries the byte count for the LengthMismatch check.
+// Up to 256 messages / the mailbox capacity per pair complete without the
+// receiver (eager, like the reference); larger ones stream through the ring and need the
+// matching recv to be in flight (rendezvous) — post the recv on another stream
+// or before the send when a rank both sends and receives large messages.
+#include <algorithm>
+
+#include "internal.h"
+
+namespace mcrdl {
+
+namespace {
+
+constexpr int kP2PThreads = 512;
+
+__device__ __forceinline__ uint8_t* mailbox(const DevComm& c, uint8_t* ws_owner, int sender) {
+  return ws_owner + 2 * c.half_bytes + int64_t(sender) * c.mbox_bytes;
+}
+
+// Last CTA of the launch advances the local stream counters. Sends and
+// receives have their own exit counters (and order chains, begin_op): a recv
+// may run concurrently with a send or a collective on another stream.
+__device__ __forceinline__ bool last_cta(const DevComm& c, int dir) {
+  __syncthreads();
+  bool last = false;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t prev = atomicAdd(&c.self->p2p_done[dir], 1u);
+    if (prev == gridDim.x - 1) {
+      *reinterpret_cast<volatile uint32_t*>(&c.self->p2p_done[dir]) = 0u;
+      last = true;
+    }
+  }
+  return last;
+}
+
+__global__ void __launch_bounds__(kP2PThreads)
+    k_send(DevComm c, Pad* peer_pad, uint8_t* peer_ws, const uint8_t* buf, int64_t bytes, int peer,
+           int K) {
+  __shared__ uint64_t s_base, s_msg;
+  __shared__ int s_err;
+  Pad* me = c.self;
+  if (threadIdx.x == 0) {
+    s_base = *reinterpret_cast<volatile uint64_t*>(&me->p2p_tx_chunks[peer]);
+    s_msg = *reinterpret_cast<volatile uint64_t*>(&me->p2p_tx_msgs[peer]);
+    s_err = 0;
+  }
+  __syncthreads();
+  const uint64_t base = s_base, msg = s_msg;
+  const int64_t nch = (bytes + kP2PChunk - 1) / kP2PChunk;
+  const int rank = c.rank;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // header slot msg % H is free once the receiver matched message msg - H
+    int e = msg >= uint64_t(kP2PHdr)
+                ? wait_geq(&me->p2p_hdr_ack[peer], me, c.timeout_ns, msg + 1 - kP2PHdr)
+                : MCRDL_OK;
+    if (e == MCRDL_OK) {
+      uint64_t* h = peer_pad->p2p_hdr[rank][msg % kP2PHdr];
+      st_relaxed_sys(&h[1], uint64_t(bytes));
+      st_release_sys(&h[0], msg + 1);
+    } else {
+      s_err = e;
+    }
+  }
+  if (blockIdx.x == 0) __syncthreads();  // every thread of the CTA sees s_err
+  uint8_t* box = mailbox(c, peer_ws, rank);
+  // (s_err is read only right after a barrier: all threads of a CTA agree)
+  for (int64_t k = blockIdx.x; k < nch; k += gridDim.x) {
+    const uint64_t g = base + uint64_t(k);
+    const int slot = int(g % uint64_t(K));
+    if (threadIdx.x == 0 && g >= uint64_t(K)) {
+      int e = wait_geq(&me->p2p_free[peer][slot], me, c.timeout_ns, g + 1 - K);
+      if (e) s_err = e;
+    }
+    __syncthreads();
+    if (s_err) break;
+    const int64_t off = k * kP2PChunk;
+    block_copy<8>(box + int64_t(slot) * kP2PChunk, buf + off, min(kP2PChunk, bytes - off));
+    __syncthreads();
+    if (threadIdx.x == 0) publish(&peer_pad->p2p_full[rank][slot], g + 1);
+  }
+  __syncthreads();
+  if (s_err && threadIdx.x == 0) raise_error(const_cast<Pad* const*>(c.pad), c.world, c.err, s_err, 0);
+  if (last_cta(c, 0)) {
+    me->p2p_tx_chunks[peer] = base + uint64_t(nch);
+    me->p2p_tx_msgs[peer] = msg + 1;
+    __threadfence();
+  }
+}
+
+__global__ void __launch_bounds__(kP2PThreads)
+    k_recv(DevComm c, Pad* peer_pad, const uint8_t* my_ws, uint8_t* buf, int64_t bytes, int peer,
+           int K) {
+  __shared__ uint64_t s_base, s_msg;
+  __shared__ int s_err;
+  Pad* me = c.self;
+  if (threadIdx.x == 0) {
+    s_base = *reinterpret_cast<volatile uint64_t*>(&me->p2p_rx_chunks[peer]);
+    s_msg = *reinterpret_cast<volatile uint64_t*>(&me->p2p_rx_msgs[peer]);
+    s_err = 0;
+  }
+  __syncthreads();
+  const uint64_t base = s_base, msg = s_msg;
+  const int64_t nch = (bytes + kP2PChunk - 1) / kP2PChunk;
+  const int rank = c.rank;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint64_t* h = me->p2p_hdr[peer][msg % kP2PHdr];
+    int e = wait_geq(&h[0], me, c.timeout_ns, msg + 1);
+    if (e == MCRDL_OK) {
+      const uint64_t sent = ld_relaxed_sys(&h[1]);
+      if (ld_relaxed_sys(&h[0]) != msg + 1) e = MCRDL_ERR_ORDER_MISMATCH;  // lapped
+      else if (sent != uint64_t(bytes)) e = MCRDL_ERR_LENGTH_MISMATCH;
+      else publish(&peer_pad->p2p_hdr_ack[rank], msg + 1);
+    }
+    s_err = e;
+  }
+  // the header check must pass before any chunk is consumed: a short sender
+  // would otherwise leave chunks of its next message in our slots
+  if (blockIdx.x == 0) __syncthreads();
+  const uint8_t* box = mailbox(c, const_cast<uint8_t*>(my_ws), peer);
+  for (int64_t k = blockIdx.x; k < nch; k += gridDim.x) {
+    const uint64_t g = base + uint64_t(k);
+    const int slot = int(g % uint64_t(K));
+    if (threadIdx.x == 0) {
+      int e = wait_geq(&me->p2p_full[peer][slot], me, c.timeout_ns, g + 1);
+      if (e) s_err = e;
+    }
+    __syncthreads();
+    if (s_err) break;
+    const int64_t off = k * kP2PChunk;
+    block_copy<8>(buf + off, box + int64_t(slot) * kP2PChunk, min(kP2PChunk, bytes - off));
+    __syncthreads();
+    if (threadIdx.x == 0) publish(&peer_pad->p2p_free[rank][slot], g + 1);
+  }
+  __syncthreads();
+  if (s_err && threadIdx.x == 0) raise_error(const_cast<Pad* const*>(c.pad), c.world, c.err, s_err, 0);
+  if (last_cta(c, 1)) {
+    me->p2p_rx_chunks[peer] = base + uint64_t(nch);
+    me->p2p_rx_msgs[peer] = msg + 1;
+    __threadfence();
+  }
+}
+
+mcrdl_status_t p2p_launch(mcrdl_comm* c, void* buf, uint64_t bytes, int peer, bool is_send,
+                          void* stream_) {
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  if (peer < 0 || peer >= c->world)
+    return set_error(MCRDL_ERR_VALIDATION, "peer %d outside world %d", peer, c->world);
+  if (bytes > 0 && buf == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL buffer");
+  if (c->dc.mbox_bytes < kP2PChunk)
+    return set_error(MCRDL_ERR_UNSUPPORTED, "point-to-point mailboxes disabled (MCRDL_P2P_BYTES=0)");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  mcrdl_status_t st = begin_op(c, stream, is_send ? kChainSend : kChainRecv);
+  if (st != MCRDL_OK) return st;
+  const int K = int(c->dc.mbox_bytes / kP2PChunk);
+  const int64_t nch = int64_t((bytes + kP2PChunk - 1) / kP2PChunk);
+  // one CTA per chunk in flight, at most the ring depth and half the SMs
+  int G = int(std::min<int64_t>(std::max<int64_t>(nch, 1), std::min(K, c->num_sms / 2)));
+  if (G < 1) G = 1;
+  Pad* peer_pad = c->dc.pad[peer];
+  if (is_send) {
+    k_send<<<G, kP2PThreads, 0, stream>>>(c->dc, peer_pad, c->dc.ws[peer],
+                                          static_cast<const uint8_t*>(buf), int64_t(bytes), peer, K);
+  } else {
+    k_recv<<<G, kP2PThreads, 0, stream>>>(c->dc, peer_pad, c->dc.ws[c->rank], static_cast<uint8_t*>(buf),
+                                          int64_t(bytes), peer, K);
+  }
+  count_launch();
+  MCRDL_CUDA_CHECK(cudaGetLastError());
+  return MCRDL_OK;
+}
+
+}  // namespace
+
+}  // namespace mcrdl
+
+using namespace mcrdl;
+
+extern "C" mcrdl_status_t mcrdl_send(mcrdl_comm* comm, const void* buf, uint64_t bytes, int peer,
+                                     void* stream) {
+  return p2p_launch(comm, const_cast<void*>(buf), bytes, peer, true, stream);
+}
+
+extern "C" mcrdl_status_t mcrdl_recv(mcrdl_comm* comm, void* buf, uint64_t bytes, int peer,
+                                     void* stream) {
+  return p2p_launch(comm, buf, bytes, peer, false, stream);
+}

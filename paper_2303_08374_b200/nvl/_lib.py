@@ -52,6 +52,8 @@ SIGNATURES = {
     "mcrdl_gatherv": (c_int, [_P, _P, _P, _I64P, _I64P, c_int, c_int, c_int, c_uint64, _P]),
     "mcrdl_bcast": (c_int, [_P, _P, c_uint64, c_int, c_int, c_int, c_uint64, _P]),
     "mcrdl_barrier": (c_int, [_P, c_uint64, _P]),
+    "mcrdl_send": (c_int, [_P, _P, c_uint64, c_int, _P]),
+    "mcrdl_recv": (c_int, [_P, _P, c_uint64, c_int, _P]),
     "mcrdl_fusion_pack": (c_int, [_P, _P, _P, c_int, _P, _P]),
     "mcrdl_fusion_unpack": (c_int, [_P, _P, _P, _P, c_int, _P]),
     "mcrdl_all_reduce_fused": (c_int, [_P, _P, _P, _P, _P, c_int, c_uint64, c_int, c_int, c_int,

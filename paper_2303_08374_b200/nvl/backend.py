@@ -25,7 +25,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from ..collectives import ALGO_CODES, AlgorithmPolicy, canonical
-from ..core import (Buffer, CommOpKind, CommRequest, CompletionEvent, DType, HandleState,
+from ..core import (P2P_KINDS, Buffer, CommOpKind, CommRequest, CompletionEvent, DType, HandleState,
                     WorkHandle)
 from ..dispatch import message_bytes
 from ..errors import (BackendFinalized, CommError, NativeBackendMissing, PendingAfterTimeout,
@@ -283,12 +283,22 @@ class NvlBackendInstance:
                 return False
         return True
 
+    def _assign_seq(self, request: CommRequest) -> None:
+        """Collectives take the next backend sequence number (runtime.py:
+        147-149), which the kernels fold into the flag signature. send/recv
+        involve two ranks only: they are matched per (sender, receiver) pair
+        on the device and must not advance the world-wide sequence."""
+        if request.kind in P2P_KINDS:
+            request.seq = 0
+            return
+        request.seq = self._seq
+        self._seq += 1
+
     def post_inline(self, request: CommRequest) -> WorkHandle:
         if self.state != "initialized":
             raise BackendFinalized(f"backend {self.name!r} is {self.state}")
         with self._lock:
-            request.seq = self._seq
-            self._seq += 1
+            self._assign_seq(request)
             self._launch(request, _Direct(self.device), _raw_stream(self.device))
             self.collectives_executed += 1
         return WorkHandle.completed(self.name, request)
@@ -298,8 +308,7 @@ class NvlBackendInstance:
             raise BackendFinalized(f"backend {self.name!r} is {self.state}")
         handle = WorkHandle(self.name, request)
         with self._lock:
-            request.seq = self._seq
-            self._seq += 1
+            self._assign_seq(request)
             handle.mark_in_progress()
             self._reap()
             if self._pipelined_ok(request):
@@ -551,6 +560,15 @@ class NvlBackendInstance:
                     o.copy_(full[rank * m:(rank + 1) * m])
                 else:
                     chk(rc)
+            return
+
+        if kind is CommOpKind.send:
+            b = st.dev(req.input)
+            chk(lib.mcrdl_send(c, _ptr(b), req.input.nbytes, req.root, s))
+            return
+        if kind is CommOpKind.recv:
+            b = st.dev(req.output, upload=False, download=True)
+            chk(lib.mcrdl_recv(c, _ptr(b), req.output.nbytes, req.root, s))
             return
 
         if kind is CommOpKind.bcast:

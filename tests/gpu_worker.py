@@ -469,6 +469,97 @@ def sc_graphs(cx: Ctx):
     del g
 
 
+def sc_p2p(cx: Ctx):
+    """send/recv (runtime.py:498-508, executed at runtime.py:244-262): ring
+    shifts over the chunk boundaries, 40 queued eager sends, a rendezvous
+    message larger than the 32 MiB mailbox (recv posted first, async), the
+    tuner's rank 0<->1 ping-pong (tuner.py:128-145), self-send, staged numpy
+    buffers, CUDA-graph replay, and LengthMismatch (runtime.py:256-260) on a
+    dedicated backend."""
+    p, r, dev = cx.p, cx.r, cx.dev
+    nxt, prv = (r + 1) % p, (r - 1) % p
+    for n in (0, 1, 1000, 131072, 131073, 3_000_001):
+        x = [values(DType.f32, n, "p2p", n, q) for q in range(p)]
+        dst = torch.full((n,), -1.0, device=dev)
+        cx.rt.send(cx.b, Buffer(to_dev(x[r], DType.f32, dev)), nxt)
+        cx.rt.recv(cx.b, Buffer(dst), prv)
+        cx.check(f"p2p/ring/{n}", from_dev(dst, DType.f32), x[prv])
+    # 40 sends queued before their receives (eager: headers and slots free)
+    xs = [[values(DType.i64, 100 + k, "p2pq", k, q) for q in range(p)] for k in range(40)]
+    for k in range(40):
+        cx.rt.send(cx.b, Buffer(to_dev(xs[k][r], DType.i64, dev)), nxt)
+    outs = [torch.zeros(100 + k, dtype=torch.int64, device=dev) for k in range(40)]
+    for k in range(40):
+        cx.rt.recv(cx.b, Buffer(outs[k]), prv)
+    for k in range(40):
+        cx.check(f"p2p/queued/{k}", from_dev(outs[k], DType.i64), xs[k][prv])
+    # rendezvous: 40 MiB + 12 B > mailbox; the recv runs on the lane stream
+    n = (10 << 20) + 3
+    x = [values(DType.f32, n, "p2pbig", q) for q in range(p)]
+    dst = torch.zeros(n, device=dev)
+    h = cx.rt.recv(cx.b, Buffer(dst), prv, async_op=True)
+    cx.rt.send(cx.b, Buffer(to_dev(x[r], DType.f32, dev)), nxt)
+    h.wait()
+    torch.cuda.current_stream().wait_stream(cx.rt._instance(cx.b).stream)
+    cx.check("p2p/rendezvous", from_dev(dst, DType.f32), x[prv])
+    # ping-pong between ranks 0 and 1, bf16 payload
+    if p >= 2 and r < 2:
+        y = [values(DType.bf16, 70000, "pp", q) for q in range(2)]
+        mine = to_dev(y[r], DType.bf16, dev)
+        got = torch.zeros_like(mine)
+        if r == 0:
+            cx.rt.send(cx.b, Buffer(mine), 1)
+            cx.rt.recv(cx.b, Buffer(got), 1)
+        else:
+            cx.rt.recv(cx.b, Buffer(got), 0)
+            cx.rt.send(cx.b, Buffer(mine), 0)
+        cx.check("p2p/pingpong", from_dev(got, DType.bf16), y[1 - r])
+    # self-send
+    z = values(DType.u8, 9999, "self", r)
+    zd = torch.zeros(9999, dtype=torch.uint8, device=dev)
+    cx.rt.send(cx.b, Buffer(to_dev(z, DType.u8, dev)), r)
+    cx.rt.recv(cx.b, Buffer(zd), r)
+    cx.check("p2p/self", from_dev(zd, DType.u8), z)
+    # staged numpy buffers (reference-style host Buffers)
+    hx = [values(DType.i32, 5000, "p2phost", q) for q in range(p)]
+    hout = np.zeros(5000, dtype=np.int32)
+    cx.rt.send(cx.b, Buffer(hx[r].copy()), nxt)
+    cx.rt.recv(cx.b, Buffer(hout), prv)
+    cx.check("p2p/host", hout, hx[prv])
+    # CUDA graph: one captured ring shift, replayed with fresh inputs
+    gi = torch.zeros(777_777, device=dev)
+    go = torch.zeros_like(gi)
+    cx.rt.send(cx.b, Buffer(gi), nxt)  # warm-up outside the capture
+    cx.rt.recv(cx.b, Buffer(go), prv)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cx.rt.send(cx.b, Buffer(gi), nxt)
+        cx.rt.recv(cx.b, Buffer(go), prv)
+    for it in range(3):
+        x = [values(DType.f32, gi.numel(), "p2pgraph", it, q) for q in range(p)]
+        gi.copy_(torch.from_numpy(x[r]))
+        g.replay()
+        torch.cuda.synchronize()
+        cx.check(f"p2p/graph{it}", from_dev(go, DType.f32), x[prv])
+    del g
+    # LengthMismatch: rank 1 posts one element more than rank 0 sends
+    if p >= 2 and r < 2:
+        if r == 0:
+            cx.rt.send("lenm", Buffer(torch.ones(100, device=dev)), 1)
+            torch.cuda.synchronize()
+        else:
+            raised = None
+            try:
+                cx.rt.recv("lenm", Buffer(torch.zeros(101, device=dev)), 0, async_op=True)
+                cx.rt.synchronize(["lenm"])
+            except Exception as exc:  # noqa: BLE001
+                raised = exc
+            cx.checked += 1
+            if type(raised).__name__ != "LengthMismatch":
+                cx.failures.append(f"p2p/length_mismatch: expected LengthMismatch, got {raised!r}")
+
+
 def sc_smoke(cx: Ctx):
     """One small invocation of each hot-path family (smoke())."""
     p, r = cx.p, cx.r
@@ -597,6 +688,7 @@ SCENARIOS = {
     "host_buffers": sc_host_buffers,
     "async_fusion": sc_async_and_fusion,
     "graphs": sc_graphs,
+    "p2p": sc_p2p,
     "order_mismatch": sc_order_mismatch,
 }
 
@@ -613,6 +705,8 @@ def main() -> int:
                                                                                max_wait=5.0))]
         if "order_mismatch" in names:
             cfgs.append(BackendConfig("mism", workspace_bytes=8 << 20))
+        if "p2p" in names:
+            cfgs.append(BackendConfig("lenm", workspace_bytes=8 << 20))
         rt.init(cfgs)
         cx = Ctx(rt, "nvl")
         for name in names:

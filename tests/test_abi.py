@@ -68,6 +68,8 @@ def test_null_communicator_is_rejected():
     lib = _lib.load()
     assert lib.mcrdl_all_reduce(None, None, None, 4, 0, 0, 0, 0, None) == 9  # not_initialized
     assert lib.mcrdl_barrier(None, 0, None) == 9
+    assert lib.mcrdl_send(None, None, 0, 0, None) == 9
+    assert lib.mcrdl_recv(None, None, 0, 0, None) == 9
     assert lib.mcrdl_comm_status(None) == 9
 
 

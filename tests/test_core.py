@@ -157,8 +157,8 @@ def test_algorithm_policy_and_reference_aliases():
     assert canonical(CommOpKind.bcast, "binomial_tree") == "direct_write"
     with pytest.raises(ValidationError):
         AlgorithmPolicy({CommOpKind.all_to_allv: "nvls"})
-    with pytest.raises(UnsupportedOperation):
-        AlgorithmPolicy().algorithm(CommOpKind.send)
+    assert AlgorithmPolicy().algorithm(CommOpKind.send) == "direct"
+    assert AlgorithmPolicy().algorithm(CommOpKind.recv) == "direct"
     dis = AlgorithmPolicy(disabled=[CommOpKind.bcast])
     assert not dis.supports(CommOpKind.bcast)
     with pytest.raises(UnsupportedOperation):

@@ -15,7 +15,8 @@ from gpu_launch import run_world  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 SCENARIOS = ["golden", "all_reduce", "all_to_allv", "all_to_all", "gathers", "bcast_scatter",
-             "reduce_family", "host_buffers", "async_fusion", "graphs", "order_mismatch"]
+             "reduce_family", "host_buffers", "async_fusion", "graphs", "p2p",
+             "order_mismatch"]
 
 
 def _ngpu():
