@@ -156,6 +156,8 @@ def bus_factor(kind: CommOpKind, p: int) -> float:
         return 2.0 * (p - 1) / p
     if kind in (CommOpKind.bcast, CommOpKind.reduce):
         return 1.0
+    if kind in (CommOpKind.send, CommOpKind.recv):
+        return 2.0  # timed as the tuner's 0<->1 ping-pong: S each way per sample
     return (p - 1) / p
 
 

@@ -1025,13 +1025,23 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
           const int64_t nv_half = int64_t(c->nvls.bytes / 2);
           uint8_t* uc = reinterpret_cast<uint8_t*>(c->nvls.uc_ptr);
           uint8_t* mc = reinterpret_cast<uint8_t*>(c->nvls.mc_ptr);
-          static const int fence = int(env_int("MCRDL_NVLS_FENCE", 1));
+          // Measured (tools/nvls_knobs.sh, profiles/nvls_knobs_r1_p4.log): the
+          // switch path peaks with ~32 CTAs per role (p=4, 256 MiB: 575 GB/s vs
+          // 497 with 98), and the per-chunk system fence before the release
+          // flag costs ~3% (multimem.st + bar.sync + st.release.sys is the
+          // ordering the CUTLASS multimem all-reduce uses as well).
+          static const int64_t nv_gp = env_int("MCRDL_NVLS_GP", 32);
+          static const int fence = int(env_int("MCRDL_NVLS_FENCE", 0));
+          const int64_t gpn = std::max<int64_t>(1, std::min<int64_t>(gp, nv_gp));
+          int64_t chpn = ((sp + gpn - 1) / gpn + 3999) / 4000;
+          if (chpn < chunk_kb * 64) chpn = chunk_kb * 64;
+          const int Gn = int(3 * gpn);
           if (vec)
-            k_ar_nvls<T, true><<<G, kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, ip, op, m, sp,
-                                                           int(gp), chp, fence, sig);
+            k_ar_nvls<T, true><<<Gn, kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, ip, op, m, sp,
+                                                            int(gpn), chpn, fence, sig);
           else
-            k_ar_nvls<T, false><<<G, kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, ip, op, m, sp,
-                                                            int(gp), chp, fence, sig);
+            k_ar_nvls<T, false><<<Gn, kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, ip, op, m, sp,
+                                                             int(gpn), chpn, fence, sig);
           launched = true;
         }
       }

@@ -560,7 +560,7 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   workspace_bytes = (workspace_bytes + 2 * c->gran - 1) / (2 * c->gran) * (2 * c->gran);
   c->ws_bytes = workspace_bytes;
   // Point-to-point mailboxes after the workspace: one ring per sender
-  // (MCRDL_P2P_BYTES per sender, multiple of 512 KiB, <= 32 MiB; 0 disables).
+  // (MCRDL_P2P_BYTES per sender, multiple of 64 KiB, <= 32 MiB; 0 disables).
   int64_t mbox = int64_t(env_int("MCRDL_P2P_BYTES", int64_t(kP2PSlots) * kP2PChunk));
   mbox = std::min<int64_t>(mbox, int64_t(kP2PSlots) * kP2PChunk) / kP2PChunk * kP2PChunk;
   if (mbox < 0) mbox = 0;

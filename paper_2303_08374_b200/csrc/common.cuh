@@ -30,8 +30,8 @@ constexpr int kMaxBlocks = 512;  // flag slots per parity
 constexpr int kThreads = 512;
 // Point-to-point mailboxes (p2p.cu): every rank owns one ring of kP2PSlots x
 // kP2PChunk bytes per sender; kP2PHdr message headers per sender.
-constexpr int kP2PSlots = 64;
-constexpr int64_t kP2PChunk = 512 << 10;
+constexpr int kP2PSlots = 512;
+constexpr int64_t kP2PChunk = 64 << 10;  // one CTA pass (512 thr x 16 B x 8)
 constexpr int kP2PHdr = 256;
 
 struct Pad {

@@ -10,8 +10,8 @@
 //    endpoints take part.
 //
 // Device design. Every rank owns, after its collective workspace, one mailbox
-// per sender: a ring of K = mbox_bytes / 512 KiB chunk slots. A message of B
-// bytes is ceil(B / 512 KiB) chunks numbered on a per-(src, dst) stream that
+// per sender: a ring of K = mbox_bytes / 64 KiB chunk slots. A message of B
+// bytes is ceil(B / 64 KiB) chunks numbered on a per-(src, dst) stream that
 // never resets (device-resident counters in the local pad, so no host state
 // changes between messages and launches replay from CUDA graphs):
 //  * sender CTA b moves chunks b, b+G, ...: waits until dst freed the slot
@@ -176,8 +176,8 @@ mcrdl_status_t p2p_launch(mcrdl_comm* c, void* buf, uint64_t bytes, int peer, bo
   if (st != MCRDL_OK) return st;
   const int K = int(c->dc.mbox_bytes / kP2PChunk);
   const int64_t nch = int64_t((bytes + kP2PChunk - 1) / kP2PChunk);
-  // one CTA per chunk in flight, at most the ring depth and half the SMs
-  int G = int(std::min<int64_t>(std::max<int64_t>(nch, 1), std::min(K, c->num_sms / 2)));
+  // one CTA per chunk in flight, at most the ring depth and one per SM
+  int G = int(std::min<int64_t>(std::max<int64_t>(nch, 1), std::min(K, c->num_sms)));
   if (G < 1) G = 1;
   Pad* peer_pad = c->dc.pad[peer];
   if (is_send) {

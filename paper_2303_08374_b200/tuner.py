@@ -128,6 +128,22 @@ def make_op(rt, backend: str, kind: CommOpKind, nbytes: int, dtype: DType):
         o = Buffer(t(m * p)) if r == 0 else None
         counts, displs = [m] * p, [k * m for k in range(p)]
         return lambda: rt.gatherv(backend, o, i, 0, counts, displs)
+    if kind in (CommOpKind.send, CommOpKind.recv):
+        # the reference's rank 0 <-> 1 ping-pong, other ranks sit out
+        # (tuner.py:128-145); the receiver posts first so messages above the
+        # mailbox stream (rendezvous) without deadlock
+        if p == 1:
+            raise ValidationError("op", "send/recv ping-pong needs two ranks")
+        a, b = Buffer(t(n)), Buffer(t(n))
+
+        def pingpong():
+            if r == 0:
+                rt.send(backend, a, 1)
+                rt.recv(backend, b, 1)
+            elif r == 1:
+                rt.recv(backend, b, 0)
+                rt.send(backend, a, 0)
+        return pingpong
     raise ValidationError("op", f"{kind.name} is not benchmarkable")
 
 
