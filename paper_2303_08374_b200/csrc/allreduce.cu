@@ -786,6 +786,143 @@ __global__ void __launch_bounds__(kThreads, 2)
   epoch_exit(c, epoch);
 }
 
+// -------------------------------------------------------------- NVLS bcast
+// The root stores every 16-byte pack ONCE into the multicast mapping and the
+// switch replicates it into every rank's NVLS buffer: root egress S instead of
+// (p-1)·S for a push broadcast. Chunk r of CTA share s is signalled by a
+// multicast release store of the flag word (same path as the data: the
+// CUTLASS multimem pattern, multimem.st + bar.sync + release). Non-roots wait
+// on their unicast view of the flag, copy the chunk out, and ack their share
+// to the root at the end: the NVLS half is free again before the root reuses
+// it two launches later. Reference: Runtime.bcast (runtime.py:528-532).
+__device__ __forceinline__ void mm_st_release_u64(uint64_t* mc, uint64_t v) {
+  asm volatile("multimem.st.release.sys.global.u64 [%0], %1;" ::"l"(mc), "l"(v) : "memory");
+}
+
+// Byte-wise pack access for unaligned user buffers and the final partial
+// pack (the protocol choice must not depend on a rank's own alignment).
+__device__ __forceinline__ uint4 ld_bytes16(const uint8_t* p, int64_t valid) {
+  uint4 v = make_uint4(0, 0, 0, 0);
+  uint8_t* b = reinterpret_cast<uint8_t*>(&v);
+  for (int k = 0; k < 16 && k < valid; ++k) b[k] = p[k];
+  return v;
+}
+__device__ __forceinline__ void st_bytes16(uint8_t* p, const uint4& v, int64_t valid) {
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+  for (int k = 0; k < 16 && k < valid; ++k) p[k] = b[k];
+}
+
+__device__ __forceinline__ void bcast_nvls_body(DevComm c, uint8_t* uc, uint8_t* mc,
+                                                const uint64_t* uc_flags, uint64_t* mc_flags,
+                                                uint8_t* buf, int64_t nbytes, int root,
+                                                int64_t chp, uint32_t epoch, uint32_t sig) {
+  __shared__ int s_err;
+  __shared__ SComm S;
+  const int rank = c.rank, world = c.world, par = epoch & 1;
+  const int s = int(blockIdx.x), G = int(gridDim.x), tid = threadIdx.x, nt = blockDim.x;
+  const int64_t npk = (nbytes + 15) / 16;
+  // full packs reachable with 16-byte accesses (0 when buf is unaligned)
+  const int64_t nfast = (reinterpret_cast<uintptr_t>(buf) & 15) ? 0 : nbytes / 16;
+  const int64_t pb = npk * s / G, pe = npk * (s + 1) / G;
+  const int rows = int((pe - pb + chp - 1) / chp);
+  if (tid == 0) s_err = 0;
+  stage_comm(c, S);
+  __syncthreads();
+  if (rank == root) {
+    for (int r = 0; r < rows; ++r) {
+      const int64_t lo = pb + int64_t(r) * chp, hi = min(pe, lo + chp);
+      const int64_t hf = max(lo, min(hi, nfast));
+      int64_t i = lo + tid;
+      for (; i + 3 * nt < hf; i += 4 * nt) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ld16(buf + (i + u * nt) * 16);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mm_st(mc + (i + u * nt) * 16, v[u]);
+      }
+      for (; i < hf; i += nt) mm_st(mc + i * 16, ld16(buf + i * 16));
+      for (i = hf + tid; i < hi; i += nt) mm_st(mc + i * 16, ld_bytes16(buf + i * 16, nbytes - i * 16));
+      __syncthreads();
+      if (tid == 0) mm_st_release_u64(mc_flags + s, make_flag(epoch, sig, uint32_t(r + 1)));
+    }
+    if (tid < world && tid != root) {
+      int e = wait_flag(&S.pad[rank]->flag2[par][s][tid], S.pad[rank], c.timeout_ns, c.err, epoch,
+                        sig, 1);
+      if (e) atomicCAS(&s_err, 0, e);
+    }
+    __syncthreads();
+    if (s_err && tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+    return;
+  }
+  for (int r = 0; r < rows; ++r) {
+    if (tid == 0) {
+      int e = wait_flag(uc_flags + s, S.pad[rank], c.timeout_ns, c.err, epoch, sig, uint32_t(r + 1));
+      if (e) s_err = e;
+    }
+    __syncthreads();
+    if (s_err) {
+      if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+      return;
+    }
+    const int64_t lo = pb + int64_t(r) * chp, hi = min(pe, lo + chp);
+    const int64_t hf = max(lo, min(hi, nfast));
+    int64_t i = lo + tid;
+    for (; i + 3 * nt < hf; i += 4 * nt) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = ld16_cg(uc + (i + u * nt) * 16);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) st16(buf + (i + u * nt) * 16, v[u]);
+    }
+    for (; i < hf; i += nt) st16(buf + i * 16, ld16_cg(uc + i * 16));
+    for (i = hf + tid; i < hi; i += nt) st_bytes16(buf + i * 16, ld16_cg(uc + i * 16), nbytes - i * 16);
+  }
+  __syncthreads();
+  if (tid == 0) publish(&S.pad[root]->flag2[par][s][rank], make_flag(epoch, sig, 1));
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_bcast_nvls(DevComm c, uint8_t* uc, uint8_t* mc, int64_t nv_half, int64_t room, uint8_t* buf,
+                 int64_t nbytes, int root, int64_t chp, uint32_t sig) {
+  const uint32_t epoch = epoch_enter(c);
+  const int64_t hoff = int64_t(epoch & 1) * nv_half;
+  bcast_nvls_body(c, uc + hoff, mc + hoff, reinterpret_cast<const uint64_t*>(uc + hoff + room),
+                  reinterpret_cast<uint64_t*>(mc + hoff + room), buf, nbytes, root, chp, epoch, sig);
+  epoch_exit(c, epoch);
+}
+
+mcrdl_status_t launch_bcast_nvls(mcrdl_comm* c, uint8_t* buf, int64_t nbytes, int root, int dtype,
+                                 uint64_t count, uint64_t seq, cudaStream_t stream) {
+  const int64_t nv_half = int64_t(c->nvls.bytes / 2);
+  const int64_t room = (nv_half - kNvlsFlagBytes) / 256 * 256;
+  uint8_t* uc = reinterpret_cast<uint8_t*>(c->nvls.uc_ptr);
+  uint8_t* mc = reinterpret_cast<uint8_t*>(c->nvls.mc_ptr);
+  int64_t done = 0;
+  int sub = 0;
+  do {
+    const int64_t nb = std::min(nbytes - done, room);
+    mcrdl_status_t st = begin_op(c, stream);
+    if (st != MCRDL_OK) return st;
+    const uint32_t sig = op_sig(kKindBcast, dtype, sub, root, count, seq);
+    const int64_t npk = (nb + 15) / 16;
+    static const int64_t bc_ctas = env_int("MCRDL_BCAST_CTAS", 0);
+    static const int64_t bc_chunk_kb = env_int("MCRDL_BCAST_CHUNK_KB", 256);
+    // measured (tools/bcast_knobs.sh, p=4): 74 CTAs best at 16 MiB, 32 at 256 MiB
+    const int64_t gdef = nb >= (int64_t(64) << 20) ? 32 : c->num_sms / 2;
+    int64_t g = (nb + (256 << 10) - 1) / (256 << 10);
+    g = std::max<int64_t>(1, std::min<int64_t>(g, bc_ctas > 0 ? bc_ctas : gdef));
+    int64_t chp = ((npk + g - 1) / g + 3999) / 4000;  // <= 4000 chunks per share
+    if (chp < bc_chunk_kb * 64) chp = bc_chunk_kb * 64;
+    k_bcast_nvls<<<int(g), kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, room, buf + done, nb,
+                                                  root, chp, sig);
+    count_launch();
+    MCRDL_CUDA_CHECK(cudaGetLastError());
+    done += nb;
+    ++sub;
+  } while (done < nbytes);
+  return MCRDL_OK;
+}
+
 // ------------------------------------------------------------- fused (K9)
 // Members laid out back to back in a virtual packed buffer (element offsets
 // d_off[m], 16-byte aligned). One-shot protocol over the packed index space:
@@ -973,7 +1110,8 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
   if (algo == MCRDL_ALGO_ONE_SHOT && bytes > oneshot_max) algo = MCRDL_ALGO_TWO_SHOT;
 
   // Host chunking keeps every launch inside one workspace (or NVLS) half.
-  const int64_t room = (algo == MCRDL_ALGO_NVLS) ? int64_t(c->nvls.bytes / 2) : half / 2;
+  const int64_t room =
+      (algo == MCRDL_ALGO_NVLS) ? int64_t(c->nvls.bytes / 2) - kNvlsFlagBytes : half / 2;
   const int64_t chunk_elems = (algo == MCRDL_ALGO_ONE_SHOT)
                                   ? n
                                   : ((room - int64_t(world) * 1024) / int64_t(sizeof(T))) /

@@ -425,6 +425,13 @@ static mcrdl_status_t setup_nvls(mcrdl_comm* c, uint64_t bytes) {
     if (ok && map_handle(c, nv.mc_handle, bytes, &nv.mc_ptr) != MCRDL_OK) ok = 0;
     if (ok && map_handle(c, nv.mem_handle, bytes, &nv.uc_ptr) != MCRDL_OK) ok = 0;
   }
+  if (ok) {  // multicast flag words at the end of each half start at 0
+    for (int h = 0; h < 2; ++h)
+      if (cudaMemset(reinterpret_cast<uint8_t*>(nv.uc_ptr) + (h + 1) * (bytes / 2) - kNvlsFlagBytes,
+                     0, kNvlsFlagBytes) != cudaSuccess)
+        ok = 0;
+    if (cudaDeviceSynchronize() != cudaSuccess) ok = 0;
+  }
   if ((st = host_allgather(c, &ok, oks, sizeof(int))) != MCRDL_OK) return st;
   for (int r = 0; r < c->world; ++r) ok &= oks[r];
   nv.ok = ok != 0;

@@ -175,15 +175,24 @@ mcrdl_status_t mcrdl_gatherv(mcrdl_comm* c, const void* in, void* out, const int
 
 mcrdl_status_t mcrdl_bcast(mcrdl_comm* c, void* buf, uint64_t count, mcrdl_dtype_t dtype, int root,
                            mcrdl_algo_t algo, uint64_t seq, void* stream) {
-  (void)algo;
   if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   const int es = elem_size(dtype);
   if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
   if (root < 0 || root >= c->world)
     return set_error(MCRDL_ERR_VALIDATION, "root %d outside world %d", root, c->world);
   if (c->world == 1) return MCRDL_OK;
-  ExchangeSpec s = empty_spec(es, op_sig(kKindBcast, dtype, 0, root, count, seq));
   const int64_t nb = int64_t(count) * es;
+  // NVLS (switch multicast): root egress S instead of (p-1)·S. AUTO takes it
+  // above 32 MiB / (p-1) (measured crossover 4-16 MiB at p=4,
+  // profiles/bcast_r1_p4.csv). The choice uses only values every rank agrees
+  // on (the kernel copes with unaligned buffers and partial packs).
+  const bool nv_ok = c->nvls.ok && nb > 0;
+  if (nv_ok && (algo == MCRDL_ALGO_NVLS ||
+                (algo == MCRDL_ALGO_AUTO && c->world >= 3 &&
+                 nb >= (int64_t(32) << 20) / (c->world - 1))))
+    return launch_bcast_nvls(c, reinterpret_cast<uint8_t*>(buf), nb, root, int(dtype), count, seq,
+                             reinterpret_cast<cudaStream_t>(stream));
+  ExchangeSpec s = empty_spec(es, op_sig(kKindBcast, dtype, 0, root, count, seq));
   if (c->rank == root) {
     for (int r = 0; r < c->world; ++r) {
       if (r == root) continue;

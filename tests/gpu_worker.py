@@ -281,6 +281,28 @@ def sc_bcast_scatter(cx: Ctx):
             t = to_dev(ins[r], dtype, cx.dev)
             cx.rt.bcast(cx.b, Buffer(t), root)
             cx.check(f"bcast/{dtype.name}/root{root}", from_dev(t, dtype), ins[root])
+    # NVLS multicast bcast (explicit, and AUTO at >= 1 MiB): partial final
+    # packs, a buffer misaligned on one rank only, multi-chunk sizes
+    inst = cx.rt._instance(cx.b)
+    if bool(inst.comm.caps.nvls_supported) and p > 1:
+        for algo in ("nvls", "auto"):
+            inst.policy = AlgorithmPolicy({CommOpKind.bcast: algo})
+            for dtype, n in ((DType.u8, 1), (DType.u8, 17), (DType.f32, 1000), (DType.u8, (1 << 20) + 3),
+                             (DType.f32, (5 << 20) + 1), (DType.bf16, 3 << 20)):
+                for root in (0, p - 1):
+                    ins = [values(dtype, n, "bcnv", algo, dtype.name, n, root, q) for q in range(p)]
+                    t = to_dev(ins[r], dtype, cx.dev)
+                    cx.rt.bcast(cx.b, Buffer(t), root)
+                    cx.check(f"bcast/{algo}/{dtype.name}/{n}/root{root}", from_dev(t, dtype),
+                             ins[root])
+            # rank 1's buffer starts one byte into its allocation
+            n = (2 << 20) + 5
+            ins = [values(DType.u8, n, "bcnvmis", algo, q) for q in range(p)]
+            base = to_dev(np.concatenate([np.zeros(1, np.uint8), ins[r]]), DType.u8, cx.dev)
+            t = base[1:] if r == 1 else base[1:].clone()
+            cx.rt.bcast(cx.b, Buffer(t), 0)
+            cx.check(f"bcast/{algo}/misaligned", from_dev(t, DType.u8), ins[0])
+        inst.policy = AlgorithmPolicy()
     for root in range(p):
         m = 777
         src = values(DType.f32, p * m, "sc", root)
