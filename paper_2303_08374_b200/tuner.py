@@ -302,9 +302,29 @@ def nccl_times(sizes: Sequence[int], op: CommOpKind, dtype: DType, warmup: int, 
     stream = torch.cuda.current_stream(device)
     for nbytes in sizes:
         n = max(nbytes // dtype.size_bytes, 1)
+        rank = dist.get_rank()
         if op is CommOpKind.all_reduce:
             x = torch.ones(n, dtype=dtype.torch_dtype, device=device)
             fn = lambda: dist.all_reduce(x)  # noqa: E731
+        elif op is CommOpKind.bcast:
+            x = torch.ones(n, dtype=dtype.torch_dtype, device=device)
+            fn = lambda: dist.broadcast(x, 0)  # noqa: E731
+        elif op in (CommOpKind.all_gatherv, CommOpKind.all_gather):
+            m = max(n // p, 1)
+            x = torch.ones(m, dtype=dtype.torch_dtype, device=device)
+            y = torch.empty(m * p, dtype=dtype.torch_dtype, device=device)
+            fn = lambda: dist.all_gather_into_tensor(y, x)  # noqa: E731
+        elif op in (CommOpKind.send, CommOpKind.recv):
+            x = torch.ones(n, dtype=dtype.torch_dtype, device=device)
+            y = torch.empty_like(x)
+
+            def fn():
+                if rank == 0:
+                    dist.send(x, 1)
+                    dist.recv(y, 1)
+                elif rank == 1:
+                    dist.recv(y, 0)
+                    dist.send(x, 0)
         else:
             m = max(n // p, 1)
             x = torch.ones(m * p, dtype=dtype.torch_dtype, device=device)
@@ -371,7 +391,8 @@ def main(argv: Optional[List[str]] = None) -> int:
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", rt._instance("nvl").device))
         for op in cfg.ops:
-            if op in (CommOpKind.all_reduce, CommOpKind.all_to_allv):
+            if op in (CommOpKind.all_reduce, CommOpKind.all_to_allv, CommOpKind.bcast,
+                      CommOpKind.all_gatherv, CommOpKind.send):
                 nccl[op] = nccl_times(cfg.sizes, op, cfg.dtype, args.warmup, args.iters,
                                       rt._instance("nvl").device)
     if rt.rank == 0:
