@@ -83,18 +83,19 @@ __global__ void __launch_bounds__(kThreads) k_ar_oneshot(DevComm c, const T* in,
 // NVLink carries RS and AG traffic at the same time and local HBM work hides
 // under it. Senders never wait; reducers wait only for senders; gatherers
 // only for reducers: progress does not need CTA co-residency.
-template <typename T, bool VEC>
+template <typename T, bool VEC, int U = 4>
 __device__ __forceinline__ void push_packs(const T* in, int64_t n, int64_t g0, int64_t cnt,
                                            uint8_t* dst) {
-  // packs [g0, g0+cnt) of `in` -> dst (16-byte aligned, pack i at dst + 16*(i-g0))
+  // packs [g0, g0+cnt) of `in` -> dst (16-byte aligned, pack i at dst + 16*(i-g0));
+  // U packs in flight per thread
   const int tid = threadIdx.x, nt = blockDim.x;
   int64_t i = tid;
-  for (; i + 3 * nt < cnt; i += 4 * nt) {
-    uint4 v[4];
+  for (; i + (U - 1) * nt < cnt; i += U * nt) {
+    uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = load_pack<T, VEC>(in, g0 + i + u * nt, n);
+    for (int u = 0; u < U; ++u) v[u] = load_pack<T, VEC>(in, g0 + i + u * nt, n);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) st16(dst + (i + u * nt) * 16, v[u]);
+    for (int u = 0; u < U; ++u) st16(dst + (i + u * nt) * 16, v[u]);
   }
   for (; i < cnt; i += nt) st16(dst + i * 16, load_pack<T, VEC>(in, g0 + i, n));
 }
@@ -680,38 +681,56 @@ __device__ __forceinline__ void mm_st(void* mc, const uint4& v) {
 
 template <typename T, bool VEC>
 __device__ __forceinline__ void ar_nvls_body(DevComm c, uint8_t* uc, uint8_t* mc, const T* in,
-                                             T* out, int64_t n, int64_t sp, int gp, int64_t chp,
-                                             int fence, uint32_t epoch, uint32_t sig) {
+                                             T* out, int64_t n, int64_t sp, int gp, int gc, int gg,
+                                             int64_t chp, int fence, uint32_t epoch, uint32_t sig) {
+  // CTA roles: [0, gc) copiers, [gc, gc+gp) reducers (one per share),
+  // [gc+gp, gc+gp+gg) gatherers. Copier / gatherer CTA k serves shares
+  // k, k+gc (k+gg), ... row by row, so the local staging copies can run on
+  // fewer SMs than the switch reductions.
   constexpr int N = Pack<T>::N;
   __shared__ int s_err;
   __shared__ SComm S;
   const int par = epoch & 1, rank = c.rank, world = c.world;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int role = int(blockIdx.x) / gp, s = int(blockIdx.x) % gp;
+  const int bid = int(blockIdx.x);
+  const int role = bid < gc ? 0 : (bid < gc + gp ? 1 : 2);
+  const int k = role == 0 ? bid : (role == 1 ? bid - gc : bid - gc - gp);
   const int64_t npk = (n + N - 1) / N;
-  const int64_t rb = sp * s / gp, re = sp * (s + 1) / gp;
   if (tid == 0) s_err = 0;
   stage_comm(c, S);
   __syncthreads();
 
   if (role == 0) {  // ---------------------------------------------- copier
     int rows = 0;
-    for (int q = 0; q < world; ++q) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
+    for (int sh = k; sh < gp; sh += gc) {
+      const int64_t rb = sp * sh / gp, re = sp * (sh + 1) / gp;
+      for (int q = 0; q < world; ++q) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, sh));
+    }
     for (int r = 0; r < rows; ++r) {
-      for (int q = 0; q < world; ++q) {
-        const int64_t len = seg_len(npk, sp, q, rb, re);
-        const int64_t lo = int64_t(r) * chp;
-        if (lo >= len) continue;
-        const int64_t g0 = int64_t(q) * sp + rb + lo;
-        push_packs<T, VEC>(in, n, g0, min(chp, len - lo), uc + g0 * 16);
+      for (int sh = k; sh < gp; sh += gc) {
+        const int64_t rb = sp * sh / gp, re = sp * (sh + 1) / gp;
+        int my_rows = 0;
+        for (int q = 0; q < world; ++q)
+          my_rows = max(my_rows, nchunks(seg_len(npk, sp, q, rb, re), chp, sh));
+        if (r >= my_rows) continue;
+        for (int q = 0; q < world; ++q) {
+          const int64_t len = seg_len(npk, sp, q, rb, re);
+          const int64_t lo = int64_t(r) * chp;
+          if (lo >= len) continue;
+          const int64_t g0 = int64_t(q) * sp + rb + lo;
+          push_packs<T, VEC, 8>(in, n, g0, min(chp, len - lo), uc + g0 * 16);
+        }
+        __syncthreads();
+        if (tid < world)
+          publish(&S.pad[tid]->flag[par][sh][rank], make_flag(epoch, sig, uint32_t(r + 1)));
       }
-      __syncthreads();
-      if (tid < world) publish(&S.pad[tid]->flag[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
     }
     return;
   }
 
   if (role == 1) {  // --------------------------------------------- reducer
+    const int s = k;
+    const int64_t rb = sp * s / gp, re = sp * (s + 1) / gp;
     const int64_t len = seg_len(npk, sp, rank, rb, re);
     const int rows = nchunks(len, chp, s);
     for (int r = 0; r < rows; ++r) {
@@ -745,33 +764,39 @@ __device__ __forceinline__ void ar_nvls_body(DevComm c, uint8_t* uc, uint8_t* mc
 
   // ------------------------------------------------------------- gatherer
   int rows = 0;
-  for (int q = 0; q < world; ++q) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
+  for (int sh = k; sh < gp; sh += gg) {
+    const int64_t rb = sp * sh / gp, re = sp * (sh + 1) / gp;
+    for (int q = 0; q < world; ++q) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, sh));
+  }
   for (int r = 0; r < rows; ++r) {
-    if (tid < world && r < nchunks(seg_len(npk, sp, tid, rb, re), chp, s)) {
-      int e = wait_flag(&S.pad[rank]->flag2[par][s][tid], S.pad[rank], c.timeout_ns, c.err, epoch, sig,
-                        uint32_t(r + 1));
-      if (e) atomicCAS(&s_err, 0, e);
-    }
-    __syncthreads();
-    if (s_err) {
-      if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
-      return;
-    }
-    for (int q = 0; q < world; ++q) {
-      const int64_t len = seg_len(npk, sp, q, rb, re);
-      const int64_t lo = int64_t(r) * chp;
-      if (lo >= len) continue;
-      const int64_t hi = min(len, lo + chp);
-      const int64_t base = int64_t(q) * sp + rb;
-      int64_t i = lo + tid;
-      for (; i + 3 * nt < hi; i += 4 * nt) {
-        uint4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = ld16_cg(uc + (base + i + u * nt) * 16);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) store_pack<T, VEC>(out, base + i + u * nt, n, v[u]);
+    for (int sh = k; sh < gp; sh += gg) {
+      const int64_t rb = sp * sh / gp, re = sp * (sh + 1) / gp;
+      if (tid < world && r < nchunks(seg_len(npk, sp, tid, rb, re), chp, sh)) {
+        int e = wait_flag(&S.pad[rank]->flag2[par][sh][tid], S.pad[rank], c.timeout_ns, c.err, epoch,
+                          sig, uint32_t(r + 1));
+        if (e) atomicCAS(&s_err, 0, e);
       }
-      for (; i < hi; i += nt) store_pack<T, VEC>(out, base + i, n, ld16_cg(uc + (base + i) * 16));
+      __syncthreads();
+      if (s_err) {
+        if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+        return;
+      }
+      for (int q = 0; q < world; ++q) {
+        const int64_t len = seg_len(npk, sp, q, rb, re);
+        const int64_t lo = int64_t(r) * chp;
+        if (lo >= len) continue;
+        const int64_t hi = min(len, lo + chp);
+        const int64_t base = int64_t(q) * sp + rb;
+        int64_t i = lo + tid;
+        for (; i + 7 * nt < hi; i += 8 * nt) {
+          uint4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = ld16_cg(uc + (base + i + u * nt) * 16);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) store_pack<T, VEC>(out, base + i + u * nt, n, v[u]);
+        }
+        for (; i < hi; i += nt) store_pack<T, VEC>(out, base + i, n, ld16_cg(uc + (base + i) * 16));
+      }
     }
   }
 }
@@ -779,10 +804,10 @@ __device__ __forceinline__ void ar_nvls_body(DevComm c, uint8_t* uc, uint8_t* mc
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kThreads, 2)
     k_ar_nvls(DevComm c, uint8_t* uc, uint8_t* mc, int64_t nv_half, const T* in, T* out, int64_t n,
-              int64_t sp, int gp, int64_t chp, int fence, uint32_t sig) {
+              int64_t sp, int gp, int gc, int gg, int64_t chp, int fence, uint32_t sig) {
   const uint32_t epoch = epoch_enter(c);
   const int64_t hoff = int64_t(epoch & 1) * nv_half;
-  ar_nvls_body<T, VEC>(c, uc + hoff, mc + hoff, in, out, n, sp, gp, chp, fence, epoch, sig);
+  ar_nvls_body<T, VEC>(c, uc + hoff, mc + hoff, in, out, n, sp, gp, gc, gg, chp, fence, epoch, sig);
   epoch_exit(c, epoch);
 }
 
@@ -1170,16 +1195,23 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
           // ordering the CUTLASS multimem all-reduce uses as well).
           static const int64_t nv_gp = env_int("MCRDL_NVLS_GP", 32);
           static const int fence = int(env_int("MCRDL_NVLS_FENCE", 0));
+          // copier / gatherer CTAs: the staging copies are local HBM work with 8
+          // packs in flight per thread; 16 each matched or beat 32 each
+          // (profiles/nvls_roles_r1_p4.log: 592 vs 581 GB/s at 256 MiB)
+          static const int64_t nv_gc = env_int("MCRDL_NVLS_GC", 16);
+          static const int64_t nv_gg = env_int("MCRDL_NVLS_GG", 16);
           const int64_t gpn = std::max<int64_t>(1, std::min<int64_t>(gp, nv_gp));
+          const int gcn = int(std::max<int64_t>(1, std::min<int64_t>(nv_gc > 0 ? nv_gc : gpn, gpn)));
+          const int ggn = int(std::max<int64_t>(1, std::min<int64_t>(nv_gg > 0 ? nv_gg : gpn, gpn)));
           int64_t chpn = ((sp + gpn - 1) / gpn + 3999) / 4000;
           if (chpn < chunk_kb * 64) chpn = chunk_kb * 64;
-          const int Gn = int(3 * gpn);
+          const int Gn = int(gcn + gpn + ggn);
           if (vec)
             k_ar_nvls<T, true><<<Gn, kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, ip, op, m, sp,
-                                                            int(gpn), chpn, fence, sig);
+                                                            int(gpn), gcn, ggn, chpn, fence, sig);
           else
             k_ar_nvls<T, false><<<Gn, kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, ip, op, m, sp,
-                                                             int(gpn), chpn, fence, sig);
+                                                             int(gpn), gcn, ggn, chpn, fence, sig);
           launched = true;
         }
       }
