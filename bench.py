@@ -440,6 +440,27 @@ def secondary(rt, world, rank, dev, size, barrier, max_over_ranks):
         pg = None
         out["nccl_all_reduce"] = {"error": repr(exc)}
 
+    # Same all_reduce on symmetric-memory tensors (Runtime.symmetric_empty):
+    # the zero-copy kernels (NVLS multicast at p >= 3, peer loads at p = 2) —
+    # the opt-in analogue of NCCL user-buffer registration, reported beside
+    # the headline (which uses ordinary tensors).
+    if world > 1:
+        try:
+            a_s = rt.symmetric_empty("nvl", size // 4, "f32")
+            o_s = rt.symmetric_empty("nvl", size // 4, "f32")
+            a_s.normal_()
+            from paper_2303_08374_b200 import CommOpKind, CommRequest, ReduceOp
+
+            req = lambda: rt.post(CommRequest(CommOpKind.all_reduce, input=Buffer(a_s),  # noqa: E731
+                                              output=Buffer(o_s), op=ReduceOp.sum, backend="nvl"))
+            t = dev_time(req)
+            out["all_reduce_symmetric"] = {
+                "busbw_gbs": bus_bytes(world, size) / t / 1e9, "ms": t * 1e3,
+                "frac_of_900": bus_bytes(world, size) / t / 1e9 / 900.0, "bytes_per_rank": size,
+                "path": "k_ar_symm (NVLS multicast)" if world >= 3 else "k_ar_symm (peer loads)"}
+        except Exception as exc:  # noqa: BLE001
+            out["all_reduce_symmetric"] = {"error": repr(exc)}
+
     # DLRM cfg4: 26 tables, dim 128, f32, global batch 65536, uniform local batch
     tables = [len(x) for x in _array_split(26, world)]
     B = 65536

@@ -1110,6 +1110,179 @@ static int64_t ll_max_bytes() {
   return v;
 }
 
+// ------------------------------------------ symmetric zero-copy all_reduce
+// `in` and `out` lie in user symmetric allocations (mcrdl_symm_alloc) at the
+// same offsets on every rank: no workspace and no staging copies. Rank q owns
+// shard q of the packs:
+//  NVLS: multimem.ld_reduce of shard q straight from the inputs' multicast
+//        view, multimem.st straight into the outputs' (f32 / bf16 sum) —
+//        HBM traffic 2·S instead of 6·S for the staged k_ar_nvls;
+//  P2P:  ascending fold of shard q loaded from every rank's input over
+//        NVLink, stored into every rank's output (any dtype / op, bit-exact).
+// Per-CTA entry barrier (every peer entered: its input is final and nobody
+// writes a rank's output before that rank's previous work ended) and exit
+// barrier (every store into my output landed, every read of my input done).
+struct SymmArgs {
+  const uint8_t* in[kMaxRanks];
+  uint8_t* out[kMaxRanks];
+  const uint8_t* mc_in;
+  uint8_t* mc_out;
+};
+
+template <typename T, int OP, bool VEC, bool NVLS>
+__device__ __forceinline__ void ar_symm_body(DevComm c, const SymmArgs& a, int64_t n,
+                                             uint32_t epoch, uint32_t sig) {
+  constexpr int N = Pack<T>::N;
+  __shared__ int s_err;
+  __shared__ SComm S;
+  __shared__ const T* s_in[kMaxRanks];
+  __shared__ T* s_out[kMaxRanks];
+  const int par = epoch & 1, rank = c.rank, world = c.world;
+  const int s = int(blockIdx.x), G = int(gridDim.x), tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) {
+    s_err = 0;
+#pragma unroll
+    for (int r = 0; r < kMaxRanks; ++r) {
+      s_in[r] = reinterpret_cast<const T*>(a.in[r]);
+      s_out[r] = reinterpret_cast<T*>(a.out[r]);
+    }
+  }
+  stage_comm(c, S);
+  __syncthreads();
+  if (tid < world) publish(&S.pad[tid]->flag[par][s][rank], make_flag(epoch, sig, 1));
+  if (tid < world) {
+    int e = wait_flag(&S.pad[rank]->flag[par][s][tid], S.pad[rank], c.timeout_ns, c.err, epoch, sig, 1);
+    if (e) atomicCAS(&s_err, 0, e);
+  }
+  __syncthreads();
+  if (s_err) {
+    if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+    return;
+  }
+  const int64_t npk = (n + N - 1) / N;
+  const int64_t sp = (npk + world - 1) / world;
+  const int64_t q0 = min(npk, int64_t(rank) * sp), q1 = min(npk, q0 + sp);
+  const int64_t lo = q0 + (q1 - q0) * s / G, hi = q0 + (q1 - q0) * (s + 1) / G;
+  if constexpr (NVLS) {
+    int64_t i = lo + tid;
+    for (; i + 3 * nt < hi; i += 4 * nt) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = mm_ld_reduce_sum<T>(a.mc_in + (i + u * nt) * 16);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) mm_st(a.mc_out + (i + u * nt) * 16, v[u]);
+    }
+    for (; i < hi; i += nt) mm_st(a.mc_out + i * 16, mm_ld_reduce_sum<T>(a.mc_in + i * 16));
+  } else {
+    constexpr int RU = sizeof(T) == 2 ? 2 : 4;
+    for (int64_t i0 = lo + tid; i0 < hi; i0 += RU * nt) {
+      Pack<T> acc[RU];
+      uint4 v[RU];
+#pragma unroll
+      for (int u = 0; u < RU; ++u)
+        if (i0 + u * nt < hi) v[u] = load_pack<T, VEC>(s_in[0], i0 + u * nt, n);
+#pragma unroll
+      for (int u = 0; u < RU; ++u) acc[u].from_raw(v[u]);
+      for (int q = 1; q < world; ++q) {
+#pragma unroll
+        for (int u = 0; u < RU; ++u)
+          if (i0 + u * nt < hi) v[u] = load_pack<T, VEC>(s_in[q], i0 + u * nt, n);
+#pragma unroll
+        for (int u = 0; u < RU; ++u) acc[u].template fold<OP>(v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        if (i0 + u * nt >= hi) break;
+        const uint4 res = acc[u].to_raw();
+        for (int k = 0; k < world; ++k) {
+          const int q = (rank + k) % world;
+          store_pack<T, VEC>(s_out[q], i0 + u * nt, n, res);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < world) publish(&S.pad[tid]->flag2[par][s][rank], make_flag(epoch, sig, 1));
+  if (tid < world) {
+    int e = wait_flag(&S.pad[rank]->flag2[par][s][tid], S.pad[rank], c.timeout_ns, c.err, epoch, sig,
+                      1);
+    if (e) atomicCAS(&s_err, 0, e);
+  }
+  __syncthreads();
+  if (s_err && tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+}
+
+template <typename T, int OP, bool VEC, bool NVLS>
+__global__ void __launch_bounds__(kThreads) k_ar_symm(DevComm c, SymmArgs a, int64_t n, uint32_t sig) {
+  const uint32_t epoch = epoch_enter(c);
+  ar_symm_body<T, OP, VEC, NVLS>(c, a, n, epoch, sig);
+  epoch_exit(c, epoch);
+}
+
+// Returns true (and *st) when the symmetric path took the op.
+template <typename T, int OP>
+static bool try_ar_symm(mcrdl_comm* c, const T* in, T* out, int64_t n, mcrdl_algo_t algo,
+                        uint64_t seq, int dt, cudaStream_t stream, mcrdl_status_t* st) {
+  static const int64_t symm_on = env_int("MCRDL_SYMM", 1);
+  static const int64_t symm_ctas = env_int("MCRDL_SYMM_CTAS", 0);
+  const int64_t bytes = n * int64_t(sizeof(T));
+  if (!symm_on || c->world == 1 || bytes == 0) return false;
+  uint64_t oi = 0, oo = 0;
+  const Region* ri = find_symm(c, in, uint64_t(bytes), &oi);
+  const Region* ro = find_symm(c, out, uint64_t(bytes), &oo);
+  if (ri == nullptr || ro == nullptr) return false;
+  // Measured (tools: tuner --symm, profiles/symm_*_p{2,4}.log): the extra
+  // entry/exit barriers lose to LL / one-shot below ~2 MiB (8 MiB at p = 2,
+  // where one-shot stays ahead longer); explicit one_shot keeps the standard
+  // path too.
+  const int64_t min_bytes = c->world == 2 ? (int64_t(8) << 20) : (int64_t(2) << 20);
+  if (algo == MCRDL_ALGO_ONE_SHOT || (algo == MCRDL_ALGO_AUTO && bytes < min_bytes)) return false;
+  SymmArgs a{};
+  for (int q = 0; q < c->world; ++q) {
+    a.in[q] = reinterpret_cast<const uint8_t*>(ri->ptr[q]) + oi;
+    a.out[q] = reinterpret_cast<uint8_t*>(ro->ptr[q]) + oo;
+  }
+  const bool vec = ((oi | oo) & 15) == 0;
+  constexpr bool kNvlsType = (sizeof(T) == 4 && T(0.5) != T(0)) || sizeof(T) == 2;
+  // NVLS needs >= 3 ranks to pay off: at p = 2 its traffic (1.5 S per link
+  // direction) exceeds the peer path's S (355 vs 610 GB/s at 1 GiB).
+  const bool nv = kNvlsType && OP == MCRDL_SUM && ri->mc_ptr && ro->mc_ptr && vec &&
+                  bytes % 16 == 0 &&
+                  (algo == MCRDL_ALGO_NVLS || (algo == MCRDL_ALGO_AUTO && c->world >= 3));
+  if (nv) {
+    a.mc_in = reinterpret_cast<const uint8_t*>(ri->mc_ptr) + oi;
+    a.mc_out = reinterpret_cast<uint8_t*>(ro->mc_ptr) + oo;
+  }
+  // signature folds the buffer offsets: ranks passing different slices of
+  // the symmetric allocation fail with ORDER_MISMATCH instead of mixing data
+  uint32_t sig = op_sig(kKindAllReduce, dt, OP, nv ? -3 : -2, uint64_t(n), seq);
+  sig = mix32(mix32(sig, oi), oo);
+  if ((*st = begin_op(c, stream)) != MCRDL_OK) return true;
+  constexpr int N = Pack<T>::N;
+  const int64_t shard = ((n + N - 1) / N + c->world - 1) / c->world * 16;  // bytes per rank
+  // CTAs: the switch path peaks with ~32 (p = 4: 656 GB/s at 256 MiB vs 566
+  // with 148); the peer path wants every SM (576 vs 532 with 32).
+  int64_t g = (shard + (64 << 10) - 1) / (64 << 10);
+  g = std::max<int64_t>(1, std::min<int64_t>(g, symm_ctas > 0 ? symm_ctas : nv ? 32 : c->num_sms));
+  if constexpr (kNvlsType && OP == MCRDL_SUM) {
+    if (nv) {
+      k_ar_symm<T, OP, true, true><<<int(g), kThreads, 0, stream>>>(c->dc, a, n, sig);
+      count_launch();
+      *st = cudaGetLastError() == cudaSuccess ? MCRDL_OK
+                                               : set_error(MCRDL_ERR_CUDA, "k_ar_symm launch failed");
+      return true;
+    }
+  }
+  if (vec)
+    k_ar_symm<T, OP, true, false><<<int(g), kThreads, 0, stream>>>(c->dc, a, n, sig);
+  else
+    k_ar_symm<T, OP, false, false><<<int(g), kThreads, 0, stream>>>(c->dc, a, n, sig);
+  count_launch();
+  *st = cudaGetLastError() == cudaSuccess ? MCRDL_OK
+                                           : set_error(MCRDL_ERR_CUDA, "k_ar_symm launch failed");
+  return true;
+}
+
 template <typename T, int OP>
 static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mcrdl_algo_t algo,
                                uint64_t seq, int dt, cudaStream_t stream) {
@@ -1118,6 +1291,10 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
   const int64_t half = c->dc.half_bytes;
   const bool vec = ((uintptr_t(in) | uintptr_t(out)) & 15) == 0;
   if (world == 1) return launch_local_copy(out, in, n * int64_t(sizeof(T)), c->num_sms, stream);
+  {
+    mcrdl_status_t sst;
+    if (try_ar_symm<T, OP>(c, in, out, n, algo, seq, dt, stream, &sst)) return sst;
+  }
   const int64_t bytes = n * int64_t(sizeof(T));
   const int64_t oneshot_max = half / world / 256 * 256;
   if (algo == MCRDL_ALGO_AUTO) {

@@ -280,6 +280,17 @@ static mcrdl_status_t map_handle(mcrdl_comm* c, CUmemGenericAllocationHandle h, 
 }
 
 static void unmap_region(mcrdl_comm* c, Region& rg) {
+  if (rg.mc_ptr) {
+    g_drv.memUnmap(rg.mc_ptr, rg.bytes);
+    g_drv.addrFree(rg.mc_ptr, rg.bytes);
+    rg.mc_ptr = 0;
+  }
+  if (rg.mc_bound && g_drv.mcUnbind) g_drv.mcUnbind(rg.mc_handle, c->device, 0, rg.bytes);
+  rg.mc_bound = false;
+  if (rg.mc_handle) {
+    g_drv.memRelease(rg.mc_handle);
+    rg.mc_handle = 0;
+  }
   for (int r = 0; r < c->world; ++r) {
     if (rg.ptr[r]) {
       g_drv.memUnmap(rg.ptr[r], rg.bytes);
@@ -367,6 +378,63 @@ static mcrdl_status_t bcast_fd(mcrdl_comm* c, int fd, int* out_fd) {
 // its part succeeded and NVLS is enabled only if all did (so ranks never
 // disagree on the algorithm). Failure is not an error: the communicator
 // simply has no NVLS (caps.nvls_supported = 0).
+// Collective: bind every rank's physical copy of `rg` to one new multicast
+// object and map its multicast view (rg->mc_ptr). Failure to create or bind
+// is not an error: the region then stays P2P-only (mc_ptr == 0), agreed by
+// all ranks.
+static mcrdl_status_t bind_multicast(mcrdl_comm* c, Region* rg) {
+  CUmulticastObjectProp mp{};
+  mp.numDevices = unsigned(c->world);
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  mp.size = rg->bytes;
+  int ok = 1, oks[kMaxRanks];
+  int fd = -1, rfd = -1;
+  mcrdl_status_t st;
+  if (c->rank == 0 &&
+      (g_drv.mcCreate(&rg->mc_handle, &mp) != CUDA_SUCCESS ||
+       g_drv.exportHandle(&fd, rg->mc_handle, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) !=
+           CUDA_SUCCESS))
+    ok = 0;
+  if ((st = host_allgather(c, &ok, oks, sizeof(int))) != MCRDL_OK) return st;
+  if (!oks[0]) return MCRDL_OK;
+  if ((st = bcast_fd(c, fd, &rfd)) != MCRDL_OK) return st;
+  if (c->rank != 0) {
+    if (g_drv.importHandle(&rg->mc_handle, reinterpret_cast<void*>(uintptr_t(rfd)),
+                           CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) != CUDA_SUCCESS)
+      ok = 0;
+    close(rfd);
+  } else {
+    close(fd);
+  }
+  if (ok && g_drv.mcAddDevice(rg->mc_handle, c->device) != CUDA_SUCCESS) ok = 0;
+  if ((st = host_allgather(c, &ok, oks, sizeof(int))) != MCRDL_OK) return st;
+  for (int r = 0; r < c->world; ++r) ok &= oks[r];
+  if (ok && g_drv.mcBindMem(rg->mc_handle, 0, rg->local_handle, 0, rg->bytes, 0) != CUDA_SUCCESS)
+    ok = 0;
+  rg->mc_bound = ok != 0;
+  if (ok && map_handle(c, rg->mc_handle, rg->bytes, &rg->mc_ptr) != MCRDL_OK) ok = 0;
+  if ((st = host_allgather(c, &ok, oks, sizeof(int))) != MCRDL_OK) return st;
+  for (int r = 0; r < c->world; ++r) ok &= oks[r];
+  if (!ok && rg->mc_ptr) {  // some rank failed: every rank drops the view
+    g_drv.memUnmap(rg->mc_ptr, rg->bytes);
+    g_drv.addrFree(rg->mc_ptr, rg->bytes);
+    rg->mc_ptr = 0;
+  }
+  return MCRDL_OK;
+}
+
+const Region* find_symm(const mcrdl_comm* c, const void* p, uint64_t bytes, uint64_t* off) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  for (const Region& rg : c->symm) {
+    const uintptr_t base = uintptr_t(rg.ptr[c->rank]);
+    if (a >= base && a + bytes <= base + rg.bytes) {
+      *off = a - base;
+      return &rg;
+    }
+  }
+  return nullptr;
+}
+
 static mcrdl_status_t setup_nvls(mcrdl_comm* c, uint64_t bytes) {
   Nvls& nv = c->nvls;
   int ok = 1;
@@ -663,6 +731,20 @@ mcrdl_status_t mcrdl_comm_status(mcrdl_comm* c) {
 mcrdl_status_t mcrdl_symm_alloc(mcrdl_comm* c, uint64_t bytes, void** local_ptr) {
   if (c == nullptr || local_ptr == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL argument");
   if (bytes == 0) bytes = 1;
+  // With NVLS, size the region for a multicast binding (minimum granularity).
+  size_t mg = 0;
+  if (c->nvls.ok) {
+    CUmulticastObjectProp mp{};
+    mp.numDevices = unsigned(c->world);
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    mp.size = bytes;
+    static const int64_t rec = env_int("MCRDL_SYMM_MC_RECOMMENDED", 0);
+    if (g_drv.mcGranularity(&mp.size, &mp,
+                            rec ? CU_MULTICAST_GRANULARITY_RECOMMENDED
+                                : CU_MULTICAST_GRANULARITY_MINIMUM) == CUDA_SUCCESS)
+      mg = mp.size;
+    if (mg > 0) bytes = (bytes + mg - 1) / mg * mg;
+  }
   Region rg;
   mcrdl_status_t st = alloc_region(c, bytes, &rg);
   if (st != MCRDL_OK) {
@@ -670,6 +752,11 @@ mcrdl_status_t mcrdl_symm_alloc(mcrdl_comm* c, uint64_t bytes, void** local_ptr)
     return st;
   }
   MCRDL_CUDA_CHECK(cudaMemset(reinterpret_cast<void*>(rg.ptr[c->rank]), 0, rg.bytes));
+  if (c->nvls.ok && mg > 0 && (st = bind_multicast(c, &rg)) != MCRDL_OK) {
+    unmap_region(c, rg);
+    return st;
+  }
+  MCRDL_CUDA_CHECK(cudaDeviceSynchronize());
   c->symm.push_back(rg);
   *local_ptr = reinterpret_cast<void*>(rg.ptr[c->rank]);
   return MCRDL_OK;

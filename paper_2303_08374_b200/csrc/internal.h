@@ -21,6 +21,11 @@ struct Region {
   CUmemGenericAllocationHandle local_handle = 0;
   CUmemGenericAllocationHandle handles[kMaxRanks] = {};
   CUdeviceptr ptr[kMaxRanks] = {};  // rank r's region mapped here
+  // user symmetric allocations only: NVSwitch multicast view of the region
+  // (every rank's physical copy bound to one multicast object), else 0
+  CUmemGenericAllocationHandle mc_handle = 0;
+  CUdeviceptr mc_ptr = 0;
+  bool mc_bound = false;
 };
 
 // NVSwitch multicast (NVLS) buffer: one physical allocation per rank bound
@@ -90,6 +95,10 @@ void count_launch();
 // op epoch itself lives on the device (Pad::dev_epoch, common.cuh), so a
 // launch carries no per-op host state and can be replayed from a CUDA graph.
 enum : int { kChainCollective = 0, kChainSend = 1, kChainRecv = 2 };
+
+// The user symmetric allocation holding [p, p + bytes) (nullptr if none);
+// *off = p - region base. Every rank maps every rank's copy at ptr[r].
+const Region* find_symm(const mcrdl_comm* c, const void* p, uint64_t bytes, uint64_t* off);
 mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, int chain = kChainCollective);
 
 inline int64_t env_int(const char* name, int64_t dflt) {

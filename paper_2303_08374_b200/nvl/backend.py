@@ -59,10 +59,25 @@ class NvlComm:
     def status(self) -> None:
         _lib.check(self.lib.mcrdl_comm_status(self.handle))
 
+    def symm_alloc(self, nbytes: int) -> int:
+        """Collective: a peer-mapped (and, with NVLS, multicast-bound) device
+        allocation of `nbytes` on every rank; returns this rank's pointer."""
+        ptr = c_void_p()
+        _lib.check(self.lib.mcrdl_symm_alloc(self.handle, int(nbytes), byref(ptr)))
+        return int(ptr.value)
+
     def destroy(self) -> None:
         if self.handle:
             self.lib.mcrdl_comm_destroy(self.handle)
             self.handle = c_void_p()
+
+
+class _CudaBlock:
+    """__cuda_array_interface__ view of raw device bytes (zero-copy torch wrap)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
 
 
 class _PinnedPool:
@@ -221,6 +236,7 @@ class NvlBackendInstance:
         self._errors: List[BaseException] = []
         self._last_raw: Optional[int] = None  # stream of the most recent op
         self._pool = _PinnedPool()
+        self._symm_keep: list = []  # symmetric allocations (freed with the communicator)
         n_dev = torch.cuda.device_count()
         dev = config.device if config.device is not None else runtime.local_device
         if dev is None:
@@ -510,6 +526,18 @@ class NvlBackendInstance:
                 h._settle()
         with self._lock:
             self._reap()
+
+    def symmetric_empty(self, count: int, dtype: DType):
+        """Collective (same count/dtype on every rank, same order): a device
+        tensor in symmetric memory. all_reduce whose input and output both
+        live there runs zero-copy (csrc/allreduce.cu k_ar_symm: NVLS multicast
+        for f32/bf16 sums, peer loads + stores otherwise). Freed at finalize."""
+        dtype = DType.from_name(dtype) if isinstance(dtype, str) else dtype
+        nbytes = max(int(count) * dtype.size_bytes, 16)
+        ptr = self.comm.symm_alloc(nbytes)
+        raw = torch.as_tensor(_CudaBlock(ptr, nbytes), device=torch.device("cuda", self.device))
+        self._symm_keep.append(raw)
+        return raw[:int(count) * dtype.size_bytes].view(dtype.torch_dtype)
 
     def finalize(self, timeout: float) -> None:
         if self.state == "finalized":

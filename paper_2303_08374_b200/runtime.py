@@ -28,7 +28,8 @@ from .collectives import AlgorithmPolicy
 from .core import (AUTO_BACKEND, Buffer, CommOpKind, CommRequest, ReduceOp, WorkHandle,
                    check_backend_id, validate)
 from .errors import (BackendFinalized, CommError, DuplicateBackend, NotInitialized,
-                     PendingAfterTimeout, UnknownBackend, UnknownTransport, ValidationError)
+                     PendingAfterTimeout, UnknownBackend, UnknownTransport, UnsupportedOperation,
+                     ValidationError)
 from .middleware import CommLog, CompressionConfig, FusionConfig, FusionManager
 
 DEFAULT_TIMEOUT_SECS = 30.0
@@ -181,6 +182,16 @@ class Runtime:
         if inst is None:
             raise UnknownBackend(f"backend {name!r} is not registered")
         return inst
+
+    def symmetric_empty(self, backend: str, count: int, dtype="f32"):
+        """Collective: a device tensor of `count` elements in `backend`'s
+        symmetric memory (every rank calls it with the same arguments, in the
+        same order). Collectives on such tensors skip the staging workspace
+        (B200 extension; the reference has no device memory)."""
+        inst = self._instance(backend)
+        if not hasattr(inst, "symmetric_empty"):
+            raise UnsupportedOperation(f"backend {backend!r} has no symmetric memory")
+        return inst.symmetric_empty(count, dtype)
 
     def get_size(self, backend: str) -> int:
         return self._instance(backend).world_size

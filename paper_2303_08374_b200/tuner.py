@@ -41,6 +41,7 @@ class BenchConfig:
     measure_iters: int = 20
     statistic: str = "median"
     algorithms: Optional[Dict[CommOpKind, Sequence[str]]] = None
+    symmetric: bool = False  # all_reduce buffers from Runtime.symmetric_empty (zero-copy path)
 
     def __post_init__(self):
         self.ops = [CommOpKind(o) if isinstance(o, str) else o for o in self.ops]
@@ -90,8 +91,14 @@ def statistic_value(durations: Sequence[float], statistic: str) -> float:
     raise ValidationError("statistic", f"one of {STATISTICS}")
 
 
-def make_op(rt, backend: str, kind: CommOpKind, nbytes: int, dtype: DType):
-    """Closure posting one op whose canonical message size is ~nbytes."""
+_SYMM_CACHE: dict = {}
+
+
+def make_op(rt, backend: str, kind: CommOpKind, nbytes: int, dtype: DType,
+            symmetric: bool = False):
+    """Closure posting one op whose canonical message size is ~nbytes.
+    symmetric=True draws the buffers from the backend's symmetric memory
+    (one cached pair of blocks per size; collective on first use)."""
     import torch
 
     p, r = rt.world_size, rt.rank
@@ -102,6 +109,20 @@ def make_op(rt, backend: str, kind: CommOpKind, nbytes: int, dtype: DType):
 
     def t(count):
         return torch.ones(count, dtype=td, device=dev)
+
+    if symmetric and kind is CommOpKind.all_reduce:
+        key = (backend, n, dtype)
+        if key not in _SYMM_CACHE:
+            pair = [rt.symmetric_empty(backend, n, dtype) for _ in range(2)]
+            for x in pair:
+                x.fill_(1)
+            _SYMM_CACHE[key] = pair
+        a_t, o_t = _SYMM_CACHE[key]
+        a, o = Buffer(a_t), Buffer(o_t)
+        from .core import CommRequest
+
+        return lambda: rt.post(CommRequest(kind, input=a, output=o, op=ReduceOp.sum,
+                                           backend=backend))
 
     if kind is CommOpKind.all_reduce:
         a, o = Buffer(t(n)), Buffer(t(n))
@@ -210,7 +231,7 @@ def bench(rt, config: BenchConfig, backend: Optional[str] = None
                         continue  # the library would run two_shot: not a distinct cell
                     inst.policy = AlgorithmPolicy({op: algo})
                     try:
-                        fn = make_op(rt, backend, op, nbytes, config.dtype)
+                        fn = make_op(rt, backend, op, nbytes, config.dtype, config.symmetric)
                         d = time_op(rt, backend, fn, config.warmup_iters, config.measure_iters,
                                     batch=batch_for(nbytes))
                     except ValidationError as exc:
@@ -362,6 +383,8 @@ def main(argv: Optional[List[str]] = None) -> int:
     ap.add_argument("--out", default=None, help="write the tuning table here (rank 0)")
     ap.add_argument("--csv", default=None, help="write per-cell busbw CSV here (rank 0)")
     ap.add_argument("--nccl", action="store_true", help="also time torch.distributed NCCL")
+    ap.add_argument("--symm", action="store_true",
+                    help="all_reduce on symmetric-memory tensors (zero-copy kernels)")
     ap.add_argument("--algorithms", default=None,
                     help="comma list restricting the candidates (e.g. two_shot,nvls)")
     ap.add_argument("--api", action="store_true",
@@ -379,7 +402,7 @@ def main(argv: Optional[List[str]] = None) -> int:
     rt.init([BackendConfig("nvl", workspace_bytes=2 << 30)])
     cfg = BenchConfig(ops=args.ops.split(","), sizes=parse_sizes(args.sizes),
                       dtype=DType.from_name(args.dtype), warmup_iters=args.warmup,
-                      measure_iters=args.iters, statistic=args.statistic)
+                      measure_iters=args.iters, statistic=args.statistic, symmetric=args.symm)
     if args.algorithms:
         wanted = args.algorithms.split(",")
         cfg.algorithms = {op: [a for a in ALGORITHMS[op] if a in wanted] or ["auto"]

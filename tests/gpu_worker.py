@@ -582,6 +582,63 @@ def sc_p2p(cx: Ctx):
                 cx.failures.append(f"p2p/length_mismatch: expected LengthMismatch, got {raised!r}")
 
 
+def sc_symm(cx: Ctx):
+    """all_reduce on symmetric tensors (Runtime.symmetric_empty): the zero-copy
+    kernels (csrc/allreduce.cu k_ar_symm) — NVLS multicast for aligned f32/bf16
+    sums (tolerance), peer loads + ascending fold otherwise (bit-exact) — in
+    place, out of place, misaligned slices, and a symmetric input with a plain
+    output (standard path)."""
+    p, r, dev = cx.p, cx.r, cx.dev
+    inst = cx.rt._instance(cx.b)
+    A = cx.rt.symmetric_empty(cx.b, 64 << 20, "u8")
+    B = cx.rt.symmetric_empty(cx.b, 64 << 20, "u8")
+    nv = bool(inst.comm.caps.nvls_supported) and p > 1
+
+    def view(blk, dtype, n, off=0):
+        es = dtype.size_bytes
+        return blk[off * es:(off + n) * es].view(dtype.torch_dtype)
+
+    cases = [(DType.f32, "sum", "auto"), (DType.bf16, "sum", "auto"), (DType.f32, "sum", "two_shot"),
+             (DType.i64, "sum", "auto"), (DType.i32, "max", "auto"), (DType.u8, "min", "auto"),
+             (DType.f64, "prod", "auto")]
+    for dtype, op, algo in cases:
+        inst.policy = AlgorithmPolicy({CommOpKind.all_reduce: algo})
+        sizes = (1, 7, 4097, 65536 + 3) if op == "prod" else (1, 7, 4097, 65536 + 3, 1 << 20,
+                                                                (12 << 20) // dtype.size_bytes + 5)
+        for n in sizes:
+            for off in (0, 1):
+                for inplace in (True, False):
+                    gen = small_prod_values if op == "prod" else values
+                    ins = [gen(dtype, n, "symm", dtype.name, op, algo, n, off, q) for q in range(p)]
+                    want = (seqref.fold_bf16 if dtype is DType.bf16 else seqref.fold)(ins, op)
+                    src = view(A, dtype, n, off)
+                    src.copy_(to_dev(ins[r], dtype, dev))
+                    dst = src if inplace else view(B, dtype, n, off)
+                    cx.rt.post(CommRequest(CommOpKind.all_reduce, input=Buffer(src),
+                                           output=Buffer(dst), op=ReduceOp(op), backend=cx.b))
+                    zero_copy_nvls = (nv and op == "sum" and algo == "auto" and off == 0
+                                      and dtype in (DType.f32, DType.bf16)
+                                      and (n * dtype.size_bytes) % 16 == 0)
+                    tag = f"symm/{dtype.name}/{op}/{algo}/{n}/off{off}/{'in' if inplace else 'out'}"
+                    if zero_copy_nvls and dtype is DType.bf16:
+                        cx.check(tag, seqref.bf16_bits_to_f32(from_dev(dst, dtype)),
+                                 seqref.bf16_bits_to_f32(want), float_reduction=True, rtol=1e-2)
+                    elif zero_copy_nvls:
+                        cx.check(tag, from_dev(dst, dtype), want, float_reduction=True, rtol=1e-5)
+                    else:
+                        cx.check(tag, from_dev(dst, dtype), want)
+    inst.policy = AlgorithmPolicy()
+    # symmetric input, ordinary output: the standard (staged) path
+    n = 100_003
+    ins = [values(DType.i64, n, "symm-mixed", q) for q in range(p)]
+    src = view(A, DType.i64, n)
+    src.copy_(to_dev(ins[r], DType.i64, dev))
+    dst = torch.zeros(n, dtype=torch.int64, device=dev)
+    cx.rt.post(CommRequest(CommOpKind.all_reduce, input=Buffer(src), output=Buffer(dst),
+                           op=ReduceOp.sum, backend=cx.b))
+    cx.check("symm/mixed", from_dev(dst, DType.i64), seqref.fold(ins, "sum"))
+
+
 def sc_smoke(cx: Ctx):
     """One small invocation of each hot-path family (smoke())."""
     p, r = cx.p, cx.r
@@ -711,6 +768,7 @@ SCENARIOS = {
     "async_fusion": sc_async_and_fusion,
     "graphs": sc_graphs,
     "p2p": sc_p2p,
+    "symm": sc_symm,
     "order_mismatch": sc_order_mismatch,
 }
 
