@@ -52,7 +52,8 @@ enum {
   MCRDL_ERR_BOOTSTRAP = 7,         /* "bootstrap_timeout"     errors.py:46 */
   MCRDL_ERR_LENGTH_MISMATCH = 8,   /* "length_mismatch"       errors.py:62 */
   MCRDL_ERR_NOT_INITIALIZED = 9,   /* "not_initialized"       errors.py:83 */
-  MCRDL_ERR_INTERNAL = 10          /* "comm_error"                          */
+  MCRDL_ERR_INTERNAL = 10,         /* "comm_error"                          */
+  MCRDL_ERR_CODEC_MISMATCH = 11    /* "codec_mismatch"        errors.py:106 */
 };
 
 /* Element types: the reference DType (core.py:23-28) plus bf16. */
@@ -79,6 +80,17 @@ typedef enum {
   MCRDL_ALGO_NVLS = 3,         /* all_reduce / bcast through NVSwitch multicast  */
   MCRDL_ALGO_DIRECT_WRITE = 4  /* a2a(v), allgatherv, gatherv, bcast: push      */
 } mcrdl_algo_t;
+
+/* Payload codec flag, OR-ed into the `algo` argument of the movement
+ * collectives (all_to_all*, all_gatherv, gatherv, bcast): Trunc16Codec
+ * (middleware.py:43-75) fused into the exchange kernel — senders keep the top
+ * 16 bits of every f32 (sign, exponent, 7 mantissa bits) and push 2 bytes per
+ * element over NVLink, receivers widen with zero fill; a rank's own segment
+ * is copied exactly (it never crosses the transport). Ignored for non-f32
+ * payloads (CompressionConfig.active_for, middleware.py:86-95). Ranks that
+ * disagree on the codec fail with MCRDL_ERR_CODEC_MISMATCH
+ * (collectives.py:226-228, 284). */
+#define MCRDL_CODEC_TRUNC16 0x100
 
 /* Bootstrap all-gather supplied by the host runtime (the reference's star
  * bootstrap, transport.py:279-376, or a torch TCPStore). Must gather

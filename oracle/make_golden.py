@@ -16,6 +16,12 @@ Fixtures:
                           counts {0,1,7,64}, plus f32 all_reduce sums of 1000
                           elements at p=4. Arrays are stored as base64 raw
                           little-endian bytes so floats are exact.
+  trunc16.json            the reference's Trunc16Codec (middleware.py:43-75):
+                          decode(encode(x)) of specials + seeded normals, and
+                          live COMPRESSED collectives (CompressionConfig on the
+                          inproc backend) for every compressible kind at p=3.
+
+    python oracle/make_golden.py trunc16    # only trunc16.json
 """
 
 from __future__ import annotations
@@ -124,7 +130,64 @@ def live_cases() -> None:
     print("wrote", out, len(records), "cases")
 
 
+def trunc16_cases() -> None:
+    sys.path.insert(0, str(REF_SRC))
+    sys.path.insert(0, str(REF_TESTS))
+    from mcrdl import AlgorithmPolicy, BackendConfig, CommOpKind, DType, run_thread_world
+    from mcrdl.middleware import COMPRESSIBLE_KINDS, CompressionConfig, Trunc16Codec
+
+    spec = importlib.util.spec_from_file_location("ref_cases", REF_TESTS / "cases.py")
+    cases = importlib.util.module_from_spec(spec)
+    sys.modules["ref_cases"] = cases
+    spec.loader.exec_module(cases)
+
+    codec = Trunc16Codec()
+    special = np.array([0.0, -0.0, 1.0, -1.5, 3.14159265, np.inf, -np.inf, np.nan,
+                        np.finfo(np.float32).max, np.finfo(np.float32).tiny,
+                        np.float32(1.4e-45), -2.5e-42, 65504.0, 1e-3, -7.77e20], dtype=np.float32)
+    rng = np.random.default_rng(7)
+    x = np.concatenate([special, rng.standard_normal(1000).astype(np.float32) * 1e3])
+    roundtrip = codec.decode(codec.encode(x), x.size)
+
+    records = []
+    for kind in sorted(COMPRESSIBLE_KINDS, key=lambda k: k.value):
+        for count in (1, 7, 64):
+            seed = zlib.crc32(f"trunc16|{kind.value}|{count}".encode()) & 0xFFFF
+            case = cases.make_case(kind, DType.f32, count, 3, seed=seed)
+
+            def entry(rt, rank, case=case):
+                rt.init([BackendConfig("a", transport="inproc", policy=AlgorithmPolicy.naive(),
+                                       compression=CompressionConfig())])
+                req = case.build_request(rank, "a")
+                rt.post(req)
+                res = case.result_of(rank, req)
+                rt.finalize()
+                return res
+
+            res = run_thread_world(case.p, entry, timeout=60.0)
+            records.append({
+                "kind": kind.value, "p": case.p, "dtype": "f32", "count": count,
+                "root": case.root, "counts": case.counts, "displs": case.displs,
+                "sc_matrix": case.sc_matrix, "sdispls": case.sdispls, "rdispls": case.rdispls,
+                "inputs": ([[enc(b) for b in row] for row in case.inputs]
+                           if kind is CommOpKind.all_to_all else [enc(v) for v in case.inputs]),
+                "outputs": [None if r is None else
+                            ([enc(v) for v in r] if kind is CommOpKind.all_to_all else enc(r))
+                            for r in res],
+            })
+    out = OUT / "trunc16.json"
+    out.write_text(json.dumps({"generator": "oracle/make_golden.py trunc16",
+                               "reference": "mcrdl 0.1.0 Trunc16Codec + CompressionConfig",
+                               "roundtrip": {"input": enc(x), "output": enc(roundtrip)},
+                               "cases": records}))
+    print("wrote", out, len(records), "compressed cases")
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
-    selftest_dumps()
-    live_cases()
+    if sys.argv[1:] == ["trunc16"]:
+        trunc16_cases()
+    else:
+        selftest_dumps()
+        live_cases()
+        trunc16_cases()

@@ -1256,7 +1256,7 @@ static bool try_ar_symm(mcrdl_comm* c, const T* in, T* out, int64_t n, mcrdl_alg
   // signature folds the buffer offsets: ranks passing different slices of
   // the symmetric allocation fail with ORDER_MISMATCH instead of mixing data
   uint32_t sig = op_sig(kKindAllReduce, dt, OP, nv ? -3 : -2, uint64_t(n), seq);
-  sig = mix32(mix32(sig, oi), oo);
+  sig = mix32(mix32(sig, oi), oo) & ~kSigCodecBit;
   if ((*st = begin_op(c, stream)) != MCRDL_OK) return true;
   constexpr int N = Pack<T>::N;
   const int64_t shard = ((n + N - 1) / N + c->world - 1) / c->world * 16;  // bytes per rank

@@ -574,6 +574,7 @@ const char* mcrdl_status_kind(mcrdl_status_t s) {
     case MCRDL_ERR_BOOTSTRAP: return "bootstrap_timeout";
     case MCRDL_ERR_LENGTH_MISMATCH: return "length_mismatch";
     case MCRDL_ERR_NOT_INITIALIZED: return "not_initialized";
+    case MCRDL_ERR_CODEC_MISMATCH: return "codec_mismatch";
     default: return "comm_error";
   }
 }

@@ -127,6 +127,11 @@ __device__ __forceinline__ uint4 ld16_cg(const void* p) {
 }
 __device__ __forceinline__ void st16(void* p, const uint4& v) { *reinterpret_cast<uint4*>(p) = v; }
 
+// Bit 19 of the 20-bit flag signature carries the payload codec (trunc16),
+// every other bit the op hash: a flag that differs ONLY in that bit is a
+// codec disagreement (the reference's CodecMismatch), not an order mismatch.
+constexpr uint32_t kSigCodecBit = 1u << 19;
+
 __device__ __forceinline__ uint64_t make_flag(uint32_t epoch, uint32_t sig, uint32_t step) {
   return (uint64_t(epoch) << 32) | (uint64_t(sig & 0xFFFFFu) << 12) | uint64_t(step & 0xFFFu);
 }
@@ -221,7 +226,9 @@ static __device__ __noinline__ int wait_flag(const uint64_t* p, const Pad* me, u
     const uint64_t v = ld_acquire_sys(p);
     if (uint32_t(v >> 32) == epoch) {
       const uint32_t lo = uint32_t(v);
-      if ((lo >> 12) != (sig & 0xFFFFFu)) return MCRDL_ERR_ORDER_MISMATCH;
+      if ((lo >> 12) != (sig & 0xFFFFFu))
+        return (((lo >> 12) ^ sig) & 0xFFFFFu) == kSigCodecBit ? MCRDL_ERR_CODEC_MISMATCH
+                                                                : MCRDL_ERR_ORDER_MISMATCH;
       if ((lo & 0xFFFu) >= (step & 0xFFFu)) return MCRDL_OK;
     }
     if (++spins >= 32) {

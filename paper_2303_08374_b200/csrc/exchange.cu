@@ -41,6 +41,7 @@ struct XArgs {
   int esize;
   int gmax;          // communicator-wide cap on CTAs per pair
   int gp;            // CTAs per role in this launch
+  int codec;         // 1: trunc16 on peer pairs (2 wire bytes per f32)
   uint32_t sig_base;
 };
 
@@ -52,7 +53,65 @@ __device__ __host__ __forceinline__ int64_t rounds_for(int64_t bytes, int64_t sl
   return bytes <= slot ? 1 : (bytes + slot - 1) / slot;
 }
 __device__ __forceinline__ uint32_t pair_sig(uint32_t base, int64_t bytes) {
-  return mix32(base, uint64_t(bytes)) & 0xFFFFFu;
+  // user (not wire) bytes, codec bit carried through from the base
+  return (mix32(base, uint64_t(bytes)) & 0x7FFFFu) | (base & kSigCodecBit);
+}
+
+// Trunc16Codec fused into the copies (reference middleware.py:43-75): the
+// wire carries the top 16 bits of each f32 (sign, exponent, 7 mantissa
+// bits), widened back with zero fill. `wire` = 2 bytes per element; user
+// f32 buffers are at least 4-byte aligned, workspace offsets 16-byte.
+__device__ __forceinline__ void block_encode16(uint8_t* dst, const uint8_t* src, int64_t wire) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t ne = wire / 2;
+  int64_t done = 0;
+  if (((uintptr_t(dst) | uintptr_t(src)) & 15) == 0) {
+    const int64_t np = wire / 16;  // 8 elements per wire pack
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    int64_t i = tid;
+    for (; i + nt < np; i += 2 * nt) {
+      uint4 a[2], b[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        a[u] = s[2 * (i + u * nt)];
+        b[u] = s[2 * (i + u * nt) + 1];
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        d[i + u * nt] = make_uint4(__byte_perm(a[u].x, a[u].y, 0x7632), __byte_perm(a[u].z, a[u].w, 0x7632),
+                                   __byte_perm(b[u].x, b[u].y, 0x7632), __byte_perm(b[u].z, b[u].w, 0x7632));
+    }
+    for (; i < np; i += nt) {
+      const uint4 a = s[2 * i], b = s[2 * i + 1];
+      d[i] = make_uint4(__byte_perm(a.x, a.y, 0x7632), __byte_perm(a.z, a.w, 0x7632),
+                        __byte_perm(b.x, b.y, 0x7632), __byte_perm(b.z, b.w, 0x7632));
+    }
+    done = np * 8;
+  }
+  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
+  uint16_t* d16 = reinterpret_cast<uint16_t*>(dst);
+  for (int64_t e = done + tid; e < ne; e += nt) d16[e] = uint16_t(s32[e] >> 16);
+}
+
+__device__ __forceinline__ void block_decode16(uint8_t* dst, const uint8_t* src, int64_t wire) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t ne = wire / 2;
+  int64_t done = 0;
+  if (((uintptr_t(dst) | uintptr_t(src)) & 15) == 0) {
+    const int64_t np = wire / 16;
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    for (int64_t i = tid; i < np; i += nt) {
+      const uint4 w = __ldcg(s + i);
+      d[2 * i] = make_uint4(w.x << 16, w.x & 0xFFFF0000u, w.y << 16, w.y & 0xFFFF0000u);
+      d[2 * i + 1] = make_uint4(w.z << 16, w.z & 0xFFFF0000u, w.w << 16, w.w & 0xFFFF0000u);
+    }
+    done = np * 8;
+  }
+  const unsigned short* s16 = reinterpret_cast<const unsigned short*>(src);
+  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+  for (int64_t e = done + tid; e < ne; e += nt) d32[e] = uint32_t(__ldcg(s16 + e)) << 16;
 }
 // CTAs serving one pair: a function of the pair's byte count only.
 __device__ __host__ __forceinline__ int pair_ctas(int64_t bytes, int gmax) {
@@ -77,7 +136,15 @@ __device__ __forceinline__ Span span_of(int64_t B, int64_t slot, int g, int64_t 
   Span sp{0, 0, 0};
   if (s >= g || t >= rounds_for(B, slot)) return sp;
   const int64_t len = min(slot, B - t * slot);
-  byte_share(len, s, g, sp.a, sp.e);
+  // Share boundaries come from round 0 (the longest) in EVERY round: CTA s
+  // owns the same slot bytes each round, so the receiver's per-share ack of
+  // round t frees exactly what sender CTA s overwrites in round t+1 (a
+  // shorter last round must not shift shares onto bytes another receiver
+  // CTA is still landing).
+  int64_t chunk = (min(slot, B) + g - 1) / g;
+  chunk = (chunk + 15) & ~int64_t(15);
+  sp.a = min(len, int64_t(s) * chunk);
+  sp.e = min(len, sp.a + chunk);
   sp.n = int((sp.e - sp.a + ch - 1) / ch);
   if (B == 0 && s == 0 && t == 0) sp.n = 1;
   return sp;
@@ -99,7 +166,7 @@ struct PeerGeo {
 };
 
 __device__ __forceinline__ void geo_init(PeerGeo& G, const int64_t* bytes, int world, int rank,
-                                         int s, int gmax, int64_t slot) {
+                                         int s, int gmax, int64_t slot, int64_t ll_max) {
   const int tid = threadIdx.x;
   if (tid < world) {
     const int64_t B = bytes[tid];
@@ -107,7 +174,7 @@ __device__ __forceinline__ void geo_init(PeerGeo& G, const int64_t* bytes, int w
     G.g[tid] = g;
     G.ch[tid] = pair_chunk(B, g);
     // LL pairs (<= kLLMaxPairBytes, ll.cuh) are moved by CTA 0 of each role.
-    G.R[tid] = (tid != rank && s < g && B > kLLMaxPairBytes) ? rounds_for(B, slot) : 0;
+    G.R[tid] = (tid != rank && s < g && B > ll_max) ? rounds_for(B, slot) : 0;
   }
   __syncthreads();
   if (tid == 0) {
@@ -146,6 +213,8 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
   __shared__ uint8_t* s_rp[kMaxRanks];
   __shared__ int64_t s_sb[kMaxRanks];
   __shared__ int64_t s_rb[kMaxRanks];
+  __shared__ int64_t s_sw[kMaxRanks];  // wire bytes per pair (== user bytes without codec)
+  __shared__ int64_t s_rw[kMaxRanks];
   __shared__ int s_err;
   __shared__ SComm S;
   __shared__ PeerGeo G;
@@ -175,8 +244,14 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
     }
   }
   __syncthreads();
+  if (tid < world) {
+    s_sw[tid] = (a.codec && tid != rank) ? s_sb[tid] / 2 : s_sb[tid];
+    s_rw[tid] = (a.codec && tid != rank) ? s_rb[tid] / 2 : s_rb[tid];
+  }
   if (tid == 0 && s_sb[rank] != s_rb[rank]) s_err = MCRDL_ERR_VALIDATION;
   __syncthreads();
+  // LL carries small pairs unless the codec is on (LL moves raw bytes)
+  const int64_t ll_max = a.codec ? -1 : kLLMaxPairBytes;
   if (s_err) {
     if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
     return;
@@ -184,9 +259,9 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
 
   const int me = tid;  // peer index this thread handles in flag duties (tid < world)
   if (sender) {
-    if (s == 0)
+    if (s == 0 && !a.codec)
       exchange_ll_send_pairs(S.pad, rank, world, par, s_sp, s_sb, a.sig_base, epoch);
-    geo_init(G, s_sb, world, rank, s, a.gmax, slot);
+    geo_init(G, s_sw, world, rank, s, a.gmax, slot, ll_max);
     int sent = 0;  // chunks published to peer `me`
     for (int64_t t = 0; t < G.rmax; ++t) {
       if (t > 0) {  // slot reuse: receiver share s consumed round t-1
@@ -201,13 +276,17 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
           return;
         }
       }
-      geo_round(G, s_sb, world, s, slot, t);
+      geo_round(G, s_sw, world, s, slot, t);
       for (int r = 0; r < G.rows; ++r) {
         for (int k = 1; k < world; ++k) {
           const int j = (rank + k) % world;
           if (r >= G.n[j]) continue;
           const int64_t lo = G.a[j] + r * G.ch[j], hi = min(G.e[j], lo + G.ch[j]);
-          block_copy<4>(S.ws[j] + hoff + int64_t(rank) * slot + lo, s_sp[j] + t * slot + lo, hi - lo);
+          uint8_t* dst = S.ws[j] + hoff + int64_t(rank) * slot + lo;
+          if (a.codec)
+            block_encode16(dst, s_sp[j] + 2 * (t * slot + lo), hi - lo);
+          else
+            block_copy<4>(dst, s_sp[j] + t * slot + lo, hi - lo);
         }
         __syncthreads();
         if (me < world && me != rank && r < G.n[me]) {
@@ -226,7 +305,7 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
     byte_share(s_sb[rank], s, a.gp, lo, hi);
     block_copy<4>(s_rp[rank] + lo, s_sp[rank] + lo, hi - lo);
   }
-  if (s == 0) {
+  if (s == 0 && !a.codec) {
     const int e = exchange_ll_recv_pairs(S.pad, rank, world, par, s_rp, s_rb, a.sig_base, epoch,
                                          c.timeout_ns);
     if (e) {  // abort now: other threads may be polling lines that will never come
@@ -239,11 +318,11 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
     if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
     return;
   }
-  geo_init(G, s_rb, world, rank, s, a.gmax, slot);
+  geo_init(G, s_rw, world, rank, s, a.gmax, slot, ll_max);
   int got = 0;  // chunks consumed from peer `me`
   const uint8_t* my_ws = S.ws[rank] + hoff;
   for (int64_t t = 0; t < G.rmax; ++t) {
-    geo_round(G, s_rb, world, s, slot, t);
+    geo_round(G, s_rw, world, s, slot, t);
     for (int r = 0; r < G.rows; ++r) {
       if (me < world && me != rank && r < G.n[me]) {
         int e = wait_flag(&S.pad[rank]->flag[par][s][me], S.pad[rank], c.timeout_ns, c.err, epoch,
@@ -260,7 +339,10 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
         const int i = (rank - k + world) % world;
         if (r >= G.n[i]) continue;
         const int64_t lo = G.a[i] + r * G.ch[i], hi = min(G.e[i], lo + G.ch[i]);
-        block_copy<4>(s_rp[i] + t * slot + lo, my_ws + int64_t(i) * slot + lo, hi - lo);
+        if (a.codec)
+          block_decode16(s_rp[i] + 2 * (t * slot + lo), my_ws + int64_t(i) * slot + lo, hi - lo);
+        else
+          block_copy<4>(s_rp[i] + t * slot + lo, my_ws + int64_t(i) * slot + lo, hi - lo);
       }
     }
     // Round t of every pair fully landed: let senders reuse the slot.
@@ -293,7 +375,7 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   }
   mcrdl_status_t st = begin_op(c, stream);
   if (st != MCRDL_OK) return st;
-  if (try_exchange_ll(c, sp, stream, &st)) return st;
+  if (!sp.codec && try_exchange_ll(c, sp, stream, &st)) return st;
   XArgs a;
   memset(&a, 0, sizeof(a));
   for (int r = 0; r < c->world; ++r) {
@@ -308,7 +390,8 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   a.in_count = sp.in_count;
   a.out_count = sp.out_count;
   a.esize = sp.esize;
-  a.sig_base = sp.sig_base;
+  a.codec = sp.codec;
+  a.sig_base = (sp.sig_base & ~kSigCodecBit) | (sp.codec ? kSigCodecBit : 0u);
   a.slot = c->dc.half_bytes / c->world / 256 * 256;
   a.gmax = c->num_sms < kMaxBlocks ? c->num_sms : kMaxBlocks;  // 2 roles -> 2 CTAs/SM
   if (a.gmax < 1) a.gmax = 1;

@@ -16,6 +16,15 @@ static bool check_counts(const int64_t* counts, const int64_t* displs, int world
   return true;
 }
 
+// Strip the payload-codec flag from `algo` (MCRDL_CODEC_TRUNC16); the codec
+// applies to f32 payloads only (CompressionConfig.active_for,
+// middleware.py:86-95: other dtypes bypass silently).
+static int split_codec(mcrdl_algo_t* algo, mcrdl_dtype_t dtype) {
+  const int f = int(*algo);
+  *algo = mcrdl_algo_t(f & 0xFF);
+  return ((f & MCRDL_CODEC_TRUNC16) != 0 && dtype == MCRDL_F32) ? 1 : 0;
+}
+
 static ExchangeSpec empty_spec(int esize, uint32_t sig_base) {
   ExchangeSpec s;
   memset(&s, 0, sizeof(s));
@@ -34,7 +43,7 @@ mcrdl_status_t mcrdl_all_to_allv(mcrdl_comm* c, const void* in, void* out, const
                                  const int64_t* sdispls, const int64_t* rcounts,
                                  const int64_t* rdispls, mcrdl_dtype_t dtype, mcrdl_algo_t algo,
                                  uint64_t seq, void* stream) {
-  (void)algo;
+  const int codec = split_codec(&algo, dtype);
   if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   const int es = elem_size(dtype);
   if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
@@ -47,6 +56,7 @@ mcrdl_status_t mcrdl_all_to_allv(mcrdl_comm* c, const void* in, void* out, const
   if (in == out && in != nullptr && c->world > 1)
     return set_error(MCRDL_ERR_VALIDATION, "in-place all_to_allv: pass a snapshot of the input");
   ExchangeSpec s = empty_spec(es, op_sig(kKindA2AV, dtype, 0, -1, 0, seq));
+  s.codec = codec;
   int64_t ts = 0, tr = 0;
   for (int r = 0; r < c->world; ++r) {
     s.sptr[r] = reinterpret_cast<const uint8_t*>(in) + sdispls[r] * es;
@@ -63,12 +73,13 @@ mcrdl_status_t mcrdl_all_to_allv_dev(mcrdl_comm* c, const void* in, uint64_t in_
                                      uint64_t out_count, const int64_t* d_counts,
                                      mcrdl_dtype_t dtype, mcrdl_algo_t algo,
                                      uint64_t seq, void* stream) {
-  (void)algo;
+  const int codec = split_codec(&algo, dtype);
   if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   const int es = elem_size(dtype);
   if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
   if (d_counts == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL device count array");
   ExchangeSpec s = empty_spec(es, op_sig(kKindA2AV, dtype, 0, -1, 0, seq));
+  s.codec = codec;
   s.d_counts = d_counts;
   s.in_base = reinterpret_cast<const uint8_t*>(in);
   s.out_base = reinterpret_cast<uint8_t*>(out);
@@ -80,7 +91,7 @@ mcrdl_status_t mcrdl_all_to_allv_dev(mcrdl_comm* c, const void* in, uint64_t in_
 mcrdl_status_t mcrdl_all_to_all_single(mcrdl_comm* c, const void* in, void* out, uint64_t count,
                                        mcrdl_dtype_t dtype, mcrdl_algo_t algo, uint64_t seq,
                                        void* stream) {
-  (void)algo;
+  const int codec = split_codec(&algo, dtype);
   if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   const int es = elem_size(dtype);
   if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
@@ -91,6 +102,7 @@ mcrdl_status_t mcrdl_all_to_all_single(mcrdl_comm* c, const void* in, void* out,
     return set_error(MCRDL_ERR_VALIDATION, "in-place all_to_all_single: pass a snapshot of the input");
   const int64_t m = int64_t(count) / c->world;
   ExchangeSpec s = empty_spec(es, op_sig(kKindA2ASingle, dtype, 0, -1, uint64_t(m), seq));
+  s.codec = codec;
   for (int r = 0; r < c->world; ++r) {
     s.sptr[r] = reinterpret_cast<const uint8_t*>(in) + r * m * es;
     s.sbytes[r] = m * es;
@@ -104,11 +116,12 @@ mcrdl_status_t mcrdl_all_to_all_ptrs(mcrdl_comm* c, const void* const* in_ptrs,
                                      const int64_t* in_counts, void* const* out_ptrs,
                                      const int64_t* out_counts, mcrdl_dtype_t dtype,
                                      mcrdl_algo_t algo, uint64_t seq, void* stream) {
-  (void)algo;
+  const int codec = split_codec(&algo, dtype);
   if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   const int es = elem_size(dtype);
   if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
   ExchangeSpec s = empty_spec(es, op_sig(kKindA2AList, dtype, 0, -1, 0, seq));
+  s.codec = codec;
   int64_t ts = 0, tr = 0;
   for (int r = 0; r < c->world; ++r) {
     if (in_counts[r] < 0 || out_counts[r] < 0)
@@ -126,12 +139,13 @@ mcrdl_status_t mcrdl_all_to_all_ptrs(mcrdl_comm* c, const void* const* in_ptrs,
 mcrdl_status_t mcrdl_all_gatherv(mcrdl_comm* c, const void* in, void* out, const int64_t* rcounts,
                                  const int64_t* displs, mcrdl_dtype_t dtype, mcrdl_algo_t algo,
                                  uint64_t seq, void* stream) {
-  (void)algo;
+  const int codec = split_codec(&algo, dtype);
   if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   const int es = elem_size(dtype);
   if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
   if (!check_counts(rcounts, displs, c->world, "rcounts")) return MCRDL_ERR_VALIDATION;
   ExchangeSpec s = empty_spec(es, op_sig(kKindAllGatherv, dtype, 0, -1, 0, seq));
+  s.codec = codec;
   int64_t total = 0;
   for (int r = 0; r < c->world; ++r) {
     s.sptr[r] = reinterpret_cast<const uint8_t*>(in);
@@ -146,7 +160,7 @@ mcrdl_status_t mcrdl_all_gatherv(mcrdl_comm* c, const void* in, void* out, const
 mcrdl_status_t mcrdl_gatherv(mcrdl_comm* c, const void* in, void* out, const int64_t* rcounts,
                              const int64_t* displs, int root, mcrdl_dtype_t dtype, mcrdl_algo_t algo,
                              uint64_t seq, void* stream) {
-  (void)algo;
+  const int codec = split_codec(&algo, dtype);
   if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   const int es = elem_size(dtype);
   if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
@@ -156,6 +170,7 @@ mcrdl_status_t mcrdl_gatherv(mcrdl_comm* c, const void* in, void* out, const int
   if (c->rank == root && out == nullptr && rcounts[root] > 0)
     return set_error(MCRDL_ERR_VALIDATION, "root must supply the output buffer");
   ExchangeSpec s = empty_spec(es, op_sig(kKindGatherv, dtype, 0, root, 0, seq));
+  s.codec = codec;
   int64_t total = 0;
   if (c->rank == root) {
     for (int r = 0; r < c->world; ++r) {
@@ -175,6 +190,7 @@ mcrdl_status_t mcrdl_gatherv(mcrdl_comm* c, const void* in, void* out, const int
 
 mcrdl_status_t mcrdl_bcast(mcrdl_comm* c, void* buf, uint64_t count, mcrdl_dtype_t dtype, int root,
                            mcrdl_algo_t algo, uint64_t seq, void* stream) {
+  const int codec = split_codec(&algo, dtype);
   if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
   const int es = elem_size(dtype);
   if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
@@ -186,13 +202,14 @@ mcrdl_status_t mcrdl_bcast(mcrdl_comm* c, void* buf, uint64_t count, mcrdl_dtype
   // above 32 MiB / (p-1) (measured crossover 4-16 MiB at p=4,
   // profiles/bcast_r1_p4.csv). The choice uses only values every rank agrees
   // on (the kernel copes with unaligned buffers and partial packs).
-  const bool nv_ok = c->nvls.ok && nb > 0;
+  const bool nv_ok = c->nvls.ok && nb > 0 && !codec;  // the multicast path moves raw bytes
   if (nv_ok && (algo == MCRDL_ALGO_NVLS ||
                 (algo == MCRDL_ALGO_AUTO && c->world >= 3 &&
                  nb >= (int64_t(32) << 20) / (c->world - 1))))
     return launch_bcast_nvls(c, reinterpret_cast<uint8_t*>(buf), nb, root, int(dtype), count, seq,
                              reinterpret_cast<cudaStream_t>(stream));
   ExchangeSpec s = empty_spec(es, op_sig(kKindBcast, dtype, 0, root, count, seq));
+  s.codec = codec;
   if (c->rank == root) {
     for (int r = 0; r < c->world; ++r) {
       if (r == root) continue;

@@ -126,7 +126,7 @@ inline uint32_t op_sig(int kind, int dtype, int op, int root, uint64_t count, ui
   h = mix32(h, uint64_t(int64_t(root)));
   h = mix32(h, count);
   h = mix32(h, seq);
-  return h;
+  return h & ~kSigCodecBit;  // bit 19 of the flag signature is the codec flag
 }
 
 // Kind tags folded into signatures (CommOpKind order, core.py:89-104).
@@ -144,6 +144,7 @@ enum KindTag : int {
 
 // Exchange engine entry (exchange.cu): per-peer send/recv byte spans.
 struct ExchangeSpec {
+  int codec;  // 1: trunc16 on peer pairs (f32 only)
   const uint8_t* sptr[kMaxRanks];
   int64_t sbytes[kMaxRanks];
   uint8_t* rptr[kMaxRanks];

@@ -222,8 +222,9 @@ class NvlBackendInstance:
             raise NativeBackendMissing(
                 "the nvlink transport needs a CUDA device (B200); no CPU fallback exists")
         _lib.load()
-        if getattr(config, "compression", None) is not None:
-            raise UnsupportedOperation("compression middleware is not implemented on nvlink")
+        # CompressionConfig (middleware.py:78-95): the trunc16 codec runs inside
+        # the exchange kernel (MCRDL_CODEC_TRUNC16), halving NVLink bytes for f32.
+        self.compression = getattr(config, "compression", None)
         self.config = config
         self.name = config.name
         self.runtime = runtime
@@ -560,6 +561,9 @@ class NvlBackendInstance:
         else:
             algo = ALGO_CODES.get(name, 0)
         req._algorithm = _ALGO_NAMES.get(algo, "auto")
+        if self.compression is not None and self.compression.active_for(req) is not None:
+            algo |= CODEC_TRUNC16
+            req._algorithm += "+trunc16"
         chk = _lib.check
         self._last_raw = s
 
@@ -704,6 +708,7 @@ class NvlBackendInstance:
 
 
 _ALGO_NAMES = {v: k for k, v in ALGO_CODES.items()}
+CODEC_TRUNC16 = 0x100  # include/mcrdl_nvl.h MCRDL_CODEC_TRUNC16
 
 
 def _is_dev(x) -> bool:

@@ -80,6 +80,38 @@ def load_live() -> list:
     return json.loads(f.read_text())["cases"] if f.exists() else []
 
 
+def load_trunc16() -> dict:
+    f = GOLDEN / "trunc16.json"
+    return json.loads(f.read_text()) if f.exists() else {}
+
+
+def trunc16_oracle(c: dict) -> list:
+    """Oracle output per rank for one compressed (trunc16) record: rank r sees
+    trunc16 of every other rank's data and its own data exactly."""
+    p, out = c["p"], []
+    for r in range(p):
+        cc = dict(c)
+        if c["kind"] == "all_to_all":
+            cc["inputs"] = [[enc_like(seqref.trunc16(dec(b)) if q != r else dec(b)) for b in row]
+                            for q, row in enumerate(c["inputs"])]
+        elif c["kind"] in ("scatter", "scatterv"):  # inputs[0] holds the root's data
+            x = dec(c["inputs"][0])
+            cc["inputs"] = [enc_like(seqref.trunc16(x) if r != c["root"] else x)] + c["inputs"][1:]
+        else:
+            cc["inputs"] = [enc_like(seqref.trunc16(dec(x)) if q != r else dec(x))
+                            for q, x in enumerate(c["inputs"])]
+        cc["op"] = "sum"
+        out.append(live_oracle(cc)[r])
+    return out
+
+
+def enc_like(a: np.ndarray) -> dict:
+    import base64
+
+    a = np.ascontiguousarray(a)
+    return {"dtype": a.dtype.str, "b64": base64.b64encode(a.tobytes()).decode()}
+
+
 def live_oracle(c: dict) -> list:
     """Oracle output per rank for one live_cases.json record."""
     kind, p, root, op = c["kind"], c["p"], c["root"], c["op"]

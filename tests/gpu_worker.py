@@ -26,7 +26,8 @@ import torch  # noqa: E402
 
 import paper_2303_08374_b200 as mc  # noqa: E402
 from paper_2303_08374_b200 import (AlgorithmPolicy, BackendConfig, Buffer, CommOpKind,  # noqa: E402
-                                   CommRequest, DType, FusionConfig, ReduceOp, Runtime)
+                                   CommRequest, CompressionConfig, DType, FusionConfig, ReduceOp,
+                                   Runtime)
 from paper_2303_08374_b200.errors import OrderMismatch  # noqa: E402
 from paper_2303_08374_b200.nvl import _lib  # noqa: E402
 from oracle import seqref  # noqa: E402
@@ -212,6 +213,20 @@ def sc_all_to_allv(cx: Ctx):
     o = torch.zeros(sum(rc), dtype=torch.float32, device=cx.dev)
     cx.rt.all_to_allv(cx.b, Buffer(o), Buffer(i), sc[r], rc, sd[r], rd[r])
     cx.check("a2av/cfg1", from_dev(o, DType.f32), want[r])
+    # pairs larger than a workspace slot: acknowledged rounds with a short last
+    # round (backend "small": 16 MiB workspace)
+    for count in (1_500_000, 3_000_001):
+        sc = counts_matrix(p, count, "a2av-rounds", count)
+        sd = [packed(row) for row in sc]
+        rd = [packed([sc[j][q] for j in range(p)]) for q in range(p)]
+        ins = [values(DType.f32, sum(sc[q]), "a2av-rounds-in", count, q) for q in range(p)]
+        want = seqref.all_to_allv(ins, sc, sd, rd,
+                                  out_counts=[sum(sc[j][q] for j in range(p)) for q in range(p)])
+        rc = [sc[j][r] for j in range(p)]
+        o = torch.zeros(sum(rc), dtype=torch.float32, device=cx.dev)
+        cx.rt.all_to_allv("small", Buffer(o), Buffer(to_dev(ins[r], DType.f32, cx.dev)), sc[r], rc,
+                          sd[r], rd[r])
+        cx.check(f"a2av/rounds/{count}", from_dev(o, DType.f32), want[r])
 
 
 def sc_all_to_all(cx: Ctx):
@@ -639,6 +654,98 @@ def sc_symm(cx: Ctx):
     cx.check("symm/mixed", from_dev(dst, DType.i64), seqref.fold(ins, "sum"))
 
 
+def sc_codec(cx: Ctx):
+    """Trunc16 codec fused into the exchange kernel (CompressionConfig,
+    middleware.py:43-95): every compressible kind on backend "cmp" against the
+    oracle with peers' data truncated (seqref.trunc16) and the own segment
+    exact; non-f32 payloads bypass; misaligned f32; numpy Buffers; and ranks
+    that disagree on the codec -> CodecMismatch (collectives.py:226-228)."""
+    p, r, dev, b = cx.p, cx.r, cx.dev, "cmp"
+    T = seqref.trunc16
+
+    def mine(xs, src_rank_of=None):
+        return [x if q == r else T(x) for q, x in enumerate(xs)]
+
+    # all_to_allv: random counts (zeros included), pairs past one workspace round
+    for count in (0, 5, 1000, 70_000, 3_000_000):
+        sc = counts_matrix(p, count, "cdc-a2av", count)
+        sd = [packed(row) for row in sc]
+        rd = [packed([sc[j][q] for j in range(p)]) for q in range(p)]
+        ins = [values(DType.f32, sum(sc[q]), "cdc-a2av-in", count, q) for q in range(p)]
+        want = seqref.all_to_allv(mine(ins), sc, sd, rd,
+                                  out_counts=[sum(sc[j][q] for j in range(p)) for q in range(p)])
+        rc = [sc[j][r] for j in range(p)]
+        o = torch.zeros(sum(rc), device=dev)
+        cx.rt.all_to_allv(b, Buffer(o), Buffer(to_dev(ins[r], DType.f32, dev)), sc[r], rc, sd[r], rd[r])
+        cx.check(f"codec/a2av/{count}", from_dev(o, DType.f32), want[r])
+    # all_to_all_single, misaligned by one element on every rank
+    m = 40_001
+    ins = [values(DType.f32, p * m + 1, "cdc-a2as", q) for q in range(p)]
+    want = seqref.all_to_all_single(mine([x[1:] for x in ins]))
+    src = to_dev(ins[r], DType.f32, dev)[1:]
+    o = torch.zeros(p * m + 1, device=dev)[1:]
+    cx.rt.all_to_all_single(b, Buffer(o), Buffer(src))
+    cx.check("codec/a2a_single/misaligned", from_dev(o, DType.f32), want[r])
+    # list form
+    blocks = [[values(DType.f32, 300 + q + j, "cdc-a2al", q, j) for j in range(p)] for q in range(p)]
+    tb = [[blk if q == r else T(blk) for blk in row] for q, row in enumerate(blocks)]
+    want = seqref.all_to_all(tb)
+    outs = [Buffer(torch.zeros(300 + j + r, device=dev)) for j in range(p)]
+    cx.rt.all_to_all(b, outs, [Buffer(to_dev(x, DType.f32, dev)) for x in blocks[r]])
+    for j in range(p):
+        cx.check(f"codec/a2a_list[{j}]", from_dev(outs[j].array, DType.f32), want[r][j])
+    # all_gatherv / gatherv / scatterv / bcast
+    counts = [5000 * (q + 1) + 3 for q in range(p)]
+    displs = packed(counts)
+    ins = [values(DType.f32, counts[q], "cdc-agv", q) for q in range(p)]
+    o = torch.zeros(sum(counts), device=dev)
+    cx.rt.all_gatherv(b, Buffer(o), Buffer(to_dev(ins[r], DType.f32, dev)), counts, displs)
+    cx.check("codec/all_gatherv", from_dev(o, DType.f32),
+             seqref.all_gatherv(mine(ins), counts, displs)[r])
+    root = p - 1
+    o = torch.zeros(sum(counts), device=dev) if r == root else None
+    cx.rt.gatherv(b, Buffer(o) if o is not None else None, Buffer(to_dev(ins[r], DType.f32, dev)),
+                  root, counts, displs)
+    if r == root:
+        cx.check("codec/gatherv", from_dev(o, DType.f32),
+                 seqref.gatherv(mine(ins), root, counts, displs)[root])
+    src = values(DType.f32, sum(counts), "cdc-scv")
+    o = torch.zeros(counts[r], device=dev)
+    cx.rt.scatterv(b, Buffer(o), Buffer(to_dev(src, DType.f32, dev)) if r == 0 else None, 0,
+                   counts, displs)
+    cx.check("codec/scatterv", from_dev(o, DType.f32),
+             seqref.scatterv(src if r == 0 else T(src), counts, displs)[r])
+    for n in (1, 777, (3 << 20) + 1):
+        ins = [values(DType.f32, n, "cdc-bc", n, q) for q in range(p)]
+        t = to_dev(ins[r], DType.f32, dev)
+        cx.rt.bcast(b, Buffer(t), 0)
+        cx.check(f"codec/bcast/{n}", from_dev(t, DType.f32), ins[0] if r == 0 else T(ins[0]))
+    # non-f32 payloads bypass the codec (exact)
+    ins = [values(DType.i64, p * 999, "cdc-i64", q) for q in range(p)]
+    o = torch.zeros(p * 999, dtype=torch.int64, device=dev)
+    cx.rt.all_to_all_single(b, Buffer(o), Buffer(to_dev(ins[r], DType.i64, dev)))
+    cx.check("codec/i64-bypass", from_dev(o, DType.i64), seqref.all_to_all_single(ins)[r])
+    # reference-style numpy Buffers (staged) through the compressed kernel
+    ins = [values(DType.f32, p * 4096, "cdc-np", q) for q in range(p)]
+    hout = np.zeros(p * 4096, dtype=np.float32)
+    cx.rt.all_to_all_single(b, Buffer(hout), Buffer(ins[r].copy()))
+    cx.check("codec/numpy", hout, seqref.all_to_all_single(mine(ins))[r])
+    # ranks disagreeing on the codec (rank 0 compresses on "cm"): CodecMismatch
+    if p >= 2:
+        n = p * 100_000  # bulk-sized pairs (the LL path carries no codec)
+        x = torch.ones(n, device=dev)
+        y = torch.zeros(n, device=dev)
+        raised = None
+        try:
+            cx.rt.all_to_all_single("cm", Buffer(y), Buffer(x), async_op=True)
+            cx.rt.synchronize(["cm"])
+        except Exception as exc:  # noqa: BLE001
+            raised = exc
+        cx.checked += 1
+        if type(raised).__name__ != "CodecMismatch":
+            cx.failures.append(f"codec/mismatch: expected CodecMismatch, got {raised!r}")
+
+
 def sc_smoke(cx: Ctx):
     """One small invocation of each hot-path family (smoke())."""
     p, r = cx.p, cx.r
@@ -769,6 +876,7 @@ SCENARIOS = {
     "graphs": sc_graphs,
     "p2p": sc_p2p,
     "symm": sc_symm,
+    "codec": sc_codec,
     "order_mismatch": sc_order_mismatch,
 }
 
@@ -785,8 +893,17 @@ def main() -> int:
                                                                                max_wait=5.0))]
         if "order_mismatch" in names:
             cfgs.append(BackendConfig("mism", workspace_bytes=8 << 20))
+        if "all_to_allv" in names:
+            cfgs.append(BackendConfig("small", workspace_bytes=16 << 20))
         if "p2p" in names:
             cfgs.append(BackendConfig("lenm", workspace_bytes=8 << 20))
+        if "codec" in names:
+            # small workspace: large pairs move in several acknowledged rounds
+            cfgs.append(BackendConfig("cmp", workspace_bytes=16 << 20,
+                                      compression=CompressionConfig()))
+            # "cm": only rank 0 compresses -> CodecMismatch on every rank
+            cfgs.append(BackendConfig("cm", workspace_bytes=64 << 20,
+                                      compression=CompressionConfig() if rank == 0 else None))
         rt.init(cfgs)
         cx = Ctx(rt, "nvl")
         for name in names:

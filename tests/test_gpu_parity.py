@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 SCENARIOS = ["golden", "all_reduce", "all_to_allv", "all_to_all", "gathers", "bcast_scatter",
              "reduce_family", "host_buffers", "async_fusion", "graphs", "p2p",
-             "symm", "order_mismatch"]
+             "symm", "codec", "order_mismatch"]
 
 
 def _ngpu():

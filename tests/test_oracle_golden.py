@@ -51,6 +51,33 @@ def test_oracle_matches_reference_live_algorithms():
     assert checked > 1500
 
 
+def test_trunc16_matches_reference_codec_and_compressed_collectives():
+    """seqref.trunc16 against the reference Trunc16Codec round trip (specials
+    included: +-0, +-inf, nan, denormals) and every compressible kind run by
+    the reference's live algorithms with CompressionConfig at p=3."""
+    g = gc.load_trunc16()
+    assert g, "tests/golden/trunc16.json missing (python oracle/make_golden.py trunc16)"
+    x, want = gc.dec(g["roundtrip"]["input"]), gc.dec(g["roundtrip"]["output"])
+    got = seqref.trunc16(x)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    checked = 0
+    for c in g["cases"]:
+        got = gc.trunc16_oracle(c)
+        for r in range(c["p"]):
+            w = c["outputs"][r]
+            if w is None:
+                continue
+            where = f"trunc16/{c['kind']}/{c['count']}/r{r}"
+            if c["kind"] == "all_to_all":
+                for j, wb in enumerate(w):
+                    assert np.array_equal(got[r][j].view(np.uint32), gc.dec(wb).view(np.uint32)), where
+            else:
+                assert np.array_equal(np.asarray(got[r]).view(np.uint32),
+                                      gc.dec(w).view(np.uint32)), where
+            checked += 1
+    assert checked >= 60
+
+
 def test_known_answers_spec_examples():
     # test_collectives.py:39-117 and frontend partner.py known answers
     assert seqref.all_reduce([np.array([r, 2 * r], np.float64) for r in range(4)],
