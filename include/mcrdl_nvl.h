@@ -129,6 +129,18 @@ mcrdl_status_t mcrdl_comm_caps(const mcrdl_comm* comm, mcrdl_caps_t* caps);
  * is poisoned after a device-detected error). */
 mcrdl_status_t mcrdl_comm_status(mcrdl_comm* comm);
 
+/* Device-timed op log (CommLog durations: the reference appends one record
+ * per completed op, runtime.py:209-230, middleware.py:100-124). Every kernel
+ * launch stamps %globaltimer at entry and exit into a host-mapped ring — no
+ * stream commands, no host sync. mcrdl_comm_log_id returns the id of the last
+ * launch issued (an op that launched kernels first..last); mcrdl_comm_op_time
+ * sets *ns to end(last) - start(first), -1 while not finished, -2 when the
+ * 4096-entry ring moved past it. Launches inside a CUDA-graph capture are not
+ * logged. */
+uint64_t mcrdl_comm_log_id(const mcrdl_comm* comm);
+mcrdl_status_t mcrdl_comm_op_time(const mcrdl_comm* comm, uint64_t first, uint64_t last,
+                                  int64_t* ns);
+
 /* Symmetric allocation (collective, same size on every rank). The returned
  * local pointer is peer-mapped, so ops whose output lies in it can be written
  * zero-copy by peers. */

@@ -532,6 +532,12 @@ mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, int chain) {
     return set_error(comm->sticky, "communicator poisoned by an earlier device error (%s)",
                      mcrdl_status_kind(comm->sticky));
   }
+  // Log id of the launch that follows (0 inside a CUDA-graph capture: replays
+  // must not stamp stale ids into the ring).
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  MCRDL_CUDA_CHECK(cudaStreamIsCapturing(stream, &cap));
+  static const int64_t log_on = env_int("MCRDL_LOG", 1);
+  comm->dc.log_id = (log_on && cap == cudaStreamCaptureStatusNone) ? ++comm->log_seq : 0;
   auto& ch = comm->chain[chain];
   if (ch.have && ch.last != stream) {
     // A stream being captured into a CUDA graph cannot wait on work outside
@@ -656,6 +662,12 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   *c->err_host = 0;
   MCRDL_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
   for (auto& ch : c->chain) MCRDL_CUDA_CHECK(cudaEventCreateWithFlags(&ch.ev, cudaEventDisableTiming));
+  {
+    const size_t lb = size_t(kOpLogSlots) * 2 * sizeof(uint64_t);
+    MCRDL_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&c->oplog_host), lb, cudaHostAllocMapped));
+    memset(c->oplog_host, 0, lb);
+    MCRDL_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dc.oplog), c->oplog_host, 0));
+  }
 #ifdef MCRDL_TRACE
   {
     const size_t tb = size_t(kMaxBlocks) * kTraceSlots * sizeof(uint64_t);
@@ -694,6 +706,7 @@ mcrdl_status_t mcrdl_comm_destroy(mcrdl_comm* c) {
   for (auto& ch : c->chain)
     if (ch.ev) cudaEventDestroy(ch.ev);
   if (c->trace_host) cudaFreeHost(c->trace_host);
+  if (c->oplog_host) cudaFreeHost(c->oplog_host);
   if (c->listen_fd >= 0) close(c->listen_fd);
   delete c;
   return MCRDL_OK;
@@ -703,6 +716,24 @@ mcrdl_status_t mcrdl_debug_trace(mcrdl_comm* c, uint64_t** host_ptr, uint64_t* s
   if (c == nullptr || host_ptr == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL argument");
   *host_ptr = c->trace_host;  // NULL unless built with --trace
   if (slots_per_cta) *slots_per_cta = kTraceSlots;
+  return MCRDL_OK;
+}
+
+uint64_t mcrdl_comm_log_id(const mcrdl_comm* c) { return c ? c->log_seq : 0; }
+
+mcrdl_status_t mcrdl_comm_op_time(const mcrdl_comm* c, uint64_t first, uint64_t last, int64_t* ns) {
+  if (c == nullptr || ns == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL argument");
+  *ns = -1;
+  if (first == 0 || last < first || c->oplog_host == nullptr) return MCRDL_OK;
+  if (c->log_seq - first >= uint64_t(kOpLogSlots)) {  // ring wrapped past it
+    *ns = -2;
+    return MCRDL_OK;
+  }
+  const uint64_t a = c->oplog_host[(first % kOpLogSlots) * 2];
+  const uint64_t b = c->oplog_host[(last % kOpLogSlots) * 2 + 1];
+  if ((a >> 48) != (first & 0xFFFF) || (b >> 48) != (last & 0xFFFF)) return MCRDL_OK;  // pending
+  const uint64_t t0 = a & 0xFFFFFFFFFFFFull, t1 = b & 0xFFFFFFFFFFFFull;
+  *ns = t1 >= t0 ? int64_t(t1 - t0) : int64_t(t1 + (1ull << 48) - t0);
   return MCRDL_OK;
 }
 

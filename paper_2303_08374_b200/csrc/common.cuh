@@ -78,6 +78,8 @@ struct DevComm {
   uint64_t timeout_ns;
   int64_t half_bytes;      // bytes per workspace half
   int64_t mbox_bytes;      // p2p mailbox per sender (at ws + 2 * half_bytes)
+  uint64_t* oplog;         // host-mapped op log ring (kOpLogSlots x {start, end} words)
+  uint64_t log_id;         // this launch's log id (0: not logged, e.g. graph capture)
   int rank;
   int world;
 };
@@ -168,8 +170,27 @@ __device__ __forceinline__ void stage_comm(const DevComm& c, SComm& s) {
 // have arrived at the exit counter, i.e. after every CTA has read the old
 // value. Launches of one comm never overlap (stream-ordered; begin_op chains
 // streams), so launch k+1 always sees launch k's store.
+// Device-timed op log (CommLog durations, reference middleware.py:100-124):
+// block 0 stamps %globaltimer at entry, the last CTA to exit at exit, into a
+// host-mapped ring — no stream commands and no fences (each stamp is ONE
+// 64-bit store: id tag in the top 16 bits, 48-bit ns time below), so logging
+// adds no latency.
+constexpr int kOpLogSlots = 4096;
+__device__ __forceinline__ uint64_t oplog_word(uint64_t id) {
+  return (id << 48) | (globaltimer_ns() & 0xFFFFFFFFFFFFull);
+}
+__device__ __forceinline__ void oplog_start(const DevComm& c) {
+  if (c.log_id != 0 && blockIdx.x == 0 && threadIdx.x == 0)
+    *reinterpret_cast<volatile uint64_t*>(c.oplog + (c.log_id % kOpLogSlots) * 2) = oplog_word(c.log_id);
+}
+__device__ __forceinline__ void oplog_end(const DevComm& c) {  // last CTA, one thread
+  if (c.log_id != 0)
+    *reinterpret_cast<volatile uint64_t*>(c.oplog + (c.log_id % kOpLogSlots) * 2 + 1) = oplog_word(c.log_id);
+}
+
 __device__ __forceinline__ uint32_t epoch_enter(const DevComm& c) {
   __shared__ uint32_t s_epoch;
+  oplog_start(c);
   if (threadIdx.x == 0) {
     const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(&c.self->dev_epoch) + 1u;
     s_epoch = e == 0u ? 1u : e;
@@ -186,6 +207,7 @@ __device__ __forceinline__ void epoch_exit(const DevComm& c, uint32_t epoch) {
       *reinterpret_cast<volatile uint32_t*>(&c.self->done_ctas) = 0u;
       *reinterpret_cast<volatile uint32_t*>(&c.self->dev_epoch) = epoch;
       __threadfence();
+      oplog_end(c);
     }
   }
 }

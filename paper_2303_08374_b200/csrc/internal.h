@@ -75,6 +75,8 @@ struct mcrdl_comm {
     bool have = false;
   } chain[3];
   uint64_t* trace_host = nullptr;  // trace builds: kMaxBlocks x kTraceSlots stamps
+  uint64_t* oplog_host = nullptr;  // kOpLogSlots x {tag0, t0, tag1, t1} (mapped)
+  uint64_t log_seq = 0;            // last log id handed to a launch
 };
 
 namespace mcrdl {

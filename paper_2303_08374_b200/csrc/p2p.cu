@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kP2PThreads)
   __shared__ uint64_t s_base, s_msg;
   __shared__ int s_err;
   Pad* me = c.self;
+  oplog_start(c);
   if (threadIdx.x == 0) {
     s_base = *reinterpret_cast<volatile uint64_t*>(&me->p2p_tx_chunks[peer]);
     s_msg = *reinterpret_cast<volatile uint64_t*>(&me->p2p_tx_msgs[peer]);
@@ -107,6 +108,7 @@ __global__ void __launch_bounds__(kP2PThreads)
     me->p2p_tx_chunks[peer] = base + uint64_t(nch);
     me->p2p_tx_msgs[peer] = msg + 1;
     __threadfence();
+    oplog_end(c);
   }
 }
 
@@ -116,6 +118,7 @@ __global__ void __launch_bounds__(kP2PThreads)
   __shared__ uint64_t s_base, s_msg;
   __shared__ int s_err;
   Pad* me = c.self;
+  oplog_start(c);
   if (threadIdx.x == 0) {
     s_base = *reinterpret_cast<volatile uint64_t*>(&me->p2p_rx_chunks[peer]);
     s_msg = *reinterpret_cast<volatile uint64_t*>(&me->p2p_rx_msgs[peer]);
@@ -160,6 +163,7 @@ __global__ void __launch_bounds__(kP2PThreads)
     me->p2p_rx_chunks[peer] = base + uint64_t(nch);
     me->p2p_rx_msgs[peer] = msg + 1;
     __threadfence();
+    oplog_end(c);
   }
 }
 

@@ -238,6 +238,7 @@ class NvlBackendInstance:
         self._last_raw: Optional[int] = None  # stream of the most recent op
         self._pool = _PinnedPool()
         self._symm_keep: list = []  # symmetric allocations (freed with the communicator)
+        self._log_pending: list = []  # (request, first log id, last log id) of inline ops
         n_dev = torch.cuda.device_count()
         dev = config.device if config.device is not None else runtime.local_device
         if dev is None:
@@ -293,8 +294,6 @@ class NvlBackendInstance:
         with no lane hop, no events and no staging (the reference's inline
         fast path, runtime.py:150-168). The C layer orders it after the
         communicator's previous op even across streams."""
-        if self.runtime.log_timing:
-            return False
         for b in request.buffers():
             if not b.is_device:
                 return False
@@ -316,9 +315,46 @@ class NvlBackendInstance:
             raise BackendFinalized(f"backend {self.name!r} is {self.state}")
         with self._lock:
             self._assign_seq(request)
+            lib, c = self.comm.lib, self.comm.handle
+            log = self.runtime.log_ops
+            if log:
+                self._drain_log(block=False)
+                first = lib.mcrdl_comm_log_id(c) + 1
             self._launch(request, _Direct(self.device), _raw_stream(self.device))
+            if log:
+                self._log_pending.append((request, first, lib.mcrdl_comm_log_id(c)))
             self.collectives_executed += 1
         return WorkHandle.completed(self.name, request)
+
+    # -------------------------------------------- device-timed CommLog records
+    def _drain_log(self, block: bool) -> None:
+        """Emit the CommLog records of finished inline ops in issue order. The
+        durations are the kernels' own %globaltimer stamps (mcrdl_comm_op_time:
+        no events on the stream). block=True (the device has drained) emits
+        everything; an op without stamps (p = 1 local copy, or a ring that
+        wrapped) is logged with a 0.001 us placeholder duration."""
+        from ..dispatch import message_bytes
+        from ..middleware import LogRecord
+
+        log = self.runtime.comm_log
+        lib, c = self.comm.lib, self.comm.handle
+        ns = ctypes.c_int64()
+        while self._log_pending:
+            req, first, last = self._log_pending[0]
+            dur = None
+            if last >= first:
+                lib.mcrdl_comm_op_time(c, first, last, ctypes.byref(ns))
+                if ns.value >= 0:
+                    dur = ns.value * 1e-3
+                elif ns.value == -1 and not block:
+                    break
+            self._log_pending.pop(0)
+            members = getattr(req, "_fused_members", 0)
+            log.emit(LogRecord(ts_us=log.now_us(), rank=self.rank, op=req.kind.value,
+                               backend=self.name, bytes=message_bytes(req, self.world_size),
+                               dur_us=max(dur or 0.0, 0.001), seq=req.seq or 0,
+                               fused=members > 0, members=members or 1,
+                               algorithm=getattr(req, "_algorithm", None)))
 
     def post(self, request: CommRequest) -> WorkHandle:
         if self.state != "initialized":
@@ -521,12 +557,14 @@ class NvlBackendInstance:
         return ce
 
     def settle(self, event: CompletionEvent) -> None:
-        """After `event` fired: settle every handle it covers."""
+        """After `event` fired: settle every handle it covers and emit the
+        CommLog records of the inline ops before it."""
         for h in getattr(event, "_pending", []):
             if not h.test():
                 h._settle()
         with self._lock:
             self._reap()
+            self._drain_log(block=True)
 
     def symmetric_empty(self, count: int, dtype: DType):
         """Collective (same count/dtype on every rank, same order): a device

@@ -95,10 +95,13 @@ class Runtime:
         self.master_port = master_port or _env_int(ENV_MASTER_PORT, default=0) or 0
         self.default_workspace_bytes = _env_int(ENV_WORKSPACE, default=DEFAULT_WORKSPACE_BYTES)
         self.comm_log = CommLog(self.rank)
-        # Device-timed CommLog records for every op (CUDA events around each
-        # op on the lane stream). Off by default: blocking device ops then
-        # take the inline path and are not logged (MCRDL_LOG_TIMING=1 to log).
-        self.log_timing = os.environ.get("MCRDL_LOG_TIMING", "0") not in ("", "0")
+        # Every completed op appends one CommLog record, as in the reference
+        # (runtime.py:209-230). Durations are DEVICE times: CUDA events around
+        # the op on its stream (inline ops: the caller's stream, finished
+        # lazily, no host sync). MCRDL_LOG=0 turns record keeping off for
+        # the lowest per-op host cost.
+        self.log_ops = os.environ.get("MCRDL_LOG", "1") not in ("", "0")
+        self.log_timing = self.log_ops  # (legacy name)
         self.tuning_table: Optional[dispatch.TuningTable] = None
         self._registry: Dict[str, object] = {}
         self._registry_lock = threading.Lock()

@@ -383,6 +383,9 @@ def main(argv: Optional[List[str]] = None) -> int:
     ap.add_argument("--out", default=None, help="write the tuning table here (rank 0)")
     ap.add_argument("--csv", default=None, help="write per-cell busbw CSV here (rank 0)")
     ap.add_argument("--nccl", action="store_true", help="also time torch.distributed NCCL")
+    ap.add_argument("--codec", action="store_true",
+                    help="backend with CompressionConfig (trunc16 fused in the exchange kernel);"
+                         " busbw counts the user (f32) bytes")
     ap.add_argument("--symm", action="store_true",
                     help="all_reduce on symmetric-memory tensors (zero-copy kernels)")
     ap.add_argument("--algorithms", default=None,
@@ -399,7 +402,10 @@ def main(argv: Optional[List[str]] = None) -> int:
 
     rt = Runtime()
     torch.cuda.set_device(rt.local_device if rt.local_device is not None else rt.rank)
-    rt.init([BackendConfig("nvl", workspace_bytes=2 << 30)])
+    from .middleware import CompressionConfig
+
+    rt.init([BackendConfig("nvl", workspace_bytes=2 << 30,
+                           compression=CompressionConfig() if args.codec else None)])
     cfg = BenchConfig(ops=args.ops.split(","), sizes=parse_sizes(args.sizes),
                       dtype=DType.from_name(args.dtype), warmup_iters=args.warmup,
                       measure_iters=args.iters, statistic=args.statistic, symmetric=args.symm)

@@ -746,6 +746,49 @@ def sc_codec(cx: Ctx):
             cx.failures.append(f"codec/mismatch: expected CodecMismatch, got {raised!r}")
 
 
+def sc_commlog(cx: Ctx):
+    """Every completed op appends one CommLog record with a DEVICE duration, as
+    the reference logs every op (runtime.py:209-230): blocking device ops via
+    deferred CUDA events on the caller's stream, async ops when their handle
+    settles; report() aggregates the flushed per-rank log (middleware.py:
+    174-215)."""
+    import tempfile
+
+    from paper_2303_08374_b200.middleware import report
+
+    p, r, dev = cx.p, cx.r, cx.dev
+    log = cx.rt.comm_log
+    cx.rt.synchronize([cx.b])
+    n0 = len(log.records())
+    t = torch.ones(1 << 20, device=dev)
+    cx.rt.all_reduce(cx.b, Buffer(t))                      # inline
+    x = torch.ones(p * 4096, device=dev)
+    y = torch.zeros_like(x)
+    cx.rt.all_to_all_single(cx.b, Buffer(y), Buffer(x))    # inline
+    h = cx.rt.all_reduce(cx.b, Buffer(torch.ones(4096, device=dev)), async_op=True)
+    h.wait()
+    cx.rt.synchronize([cx.b])
+    recs = log.records()[n0:]
+    cx.checked += 1
+    ops = sorted(rec.op for rec in recs)
+    if ops != sorted(["all_reduce", "all_to_all_single", "all_reduce"]):
+        cx.failures.append(f"commlog: records {ops}")
+    for rec in recs:
+        if not (rec.dur_us > 0 and rec.backend == cx.b and rec.rank == r):
+            cx.failures.append(f"commlog: bad record {rec}")
+        want_bytes = {"all_reduce": None, "all_to_all_single": p * 4096 * 4}.get(rec.op)
+        if want_bytes is not None and rec.bytes != want_bytes:
+            cx.failures.append(f"commlog: bytes {rec.bytes} != {want_bytes} for {rec.op}")
+    with tempfile.TemporaryDirectory() as d:
+        path = f"{d}/rank{r}.jsonl"
+        log.flush(path)
+        bd = report([path])
+        cx.checked += 1
+        rows = {(row.op, row.backend): row for row in bd.rows}
+        if ("all_reduce", cx.b) not in rows or rows[("all_reduce", cx.b)].count < 2:
+            cx.failures.append(f"commlog: report rows {bd.rows}")
+
+
 def sc_smoke(cx: Ctx):
     """One small invocation of each hot-path family (smoke())."""
     p, r = cx.p, cx.r
@@ -877,6 +920,7 @@ SCENARIOS = {
     "p2p": sc_p2p,
     "symm": sc_symm,
     "codec": sc_codec,
+    "commlog": sc_commlog,
     "order_mismatch": sc_order_mismatch,
 }
 

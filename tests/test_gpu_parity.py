@@ -16,7 +16,8 @@ pytestmark = pytest.mark.gpu
 
 SCENARIOS = ["golden", "all_reduce", "all_to_allv", "all_to_all", "gathers", "bcast_scatter",
              "reduce_family", "host_buffers", "async_fusion", "graphs", "p2p",
-             "symm", "codec", "order_mismatch"]
+             "symm", "codec", "commlog",
+             "order_mismatch"]
 
 
 def _ngpu():
