@@ -152,18 +152,67 @@ __device__ __forceinline__ void exchange_ll_body(DevComm c, LLArgs a, uint32_t e
     byte_share(a.sbytes[rank], b, G, lo, hi);
     block_copy<2>(a.rptr[rank] + lo, a.sptr[rank] + lo, hi - lo);
   }
-  for (int k = 1; k < world; ++k) {
-    const int i = (rank - k + world) % world;
-    const int64_t B = a.rbytes[i], nu = (B + 7) / 8;
-    const int e = ll_recv(ll_slot(S.pad[rank], par, i), a.rptr[i], B, nu * b / G,
-                          nu * (b + 1) / G, b == 0, mix32(a.sig_base, uint64_t(B)), epoch,
-                          S.pad[rank], c.timeout_ns);
-    if (e) {
+  // Receive: headers checked by one thread per peer in parallel; this CTA's
+  // units of every peer flattened into one index space, so each thread issues
+  // its line loads for all peers before polling any (one L2 round trip
+  // instead of one per peer).
+  __shared__ int64_t s_u0[kMaxRanks], s_cnt[kMaxRanks];
+  if (tid < world) {
+    const int64_t nu = tid == rank ? 0 : (a.rbytes[tid] + 7) / 8;
+    s_u0[tid] = nu * b / G;
+    s_cnt[tid] = nu * (b + 1) / G - nu * b / G;
+  }
+  if (b == 0 && tid < world && tid != rank) {
+    uint2 h;
+    int e = 0;
+    const uint32_t sig = mix32(a.sig_base, uint64_t(a.rbytes[tid]));
+    if (!poll_ll(ll_slot(S.pad[rank], par, tid), epoch, S.pad[rank], c.timeout_ns, h, &e)) {
       atomicCAS(&s_err, 0, e);
-      raise_error(S.pad, world, c.err, e, epoch);
-      break;
+    } else if (h.x != sig || h.y != uint32_t(a.rbytes[tid])) {
+      atomicCAS(&s_err, 0, MCRDL_ERR_ORDER_MISMATCH);
+      raise_error(S.pad, world, c.err, MCRDL_ERR_ORDER_MISMATCH, epoch);
     }
   }
+  __syncthreads();
+  int64_t total = 0;
+  for (int r = 0; r < world; ++r) total += s_cnt[r];
+  constexpr int D = 4;
+  volatile int* verr = &s_err;
+  for (int64_t base = tid; base < total && !*verr; base += int64_t(D) * blockDim.x) {
+    uint4 v[D];
+    int pi[D];
+    int64_t ui[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      int64_t idx = base + int64_t(d) * blockDim.x;
+      pi[d] = -1;
+      if (idx >= total) continue;
+      int r = 0;
+      while (idx >= s_cnt[r]) idx -= s_cnt[r++];
+      pi[d] = r;
+      ui[d] = s_u0[r] + idx;
+      v[d] = ld_ll(ll_slot(S.pad[rank], par, r) + kLLHeader + ui[d] * 16);
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      if (pi[d] < 0) continue;
+      const int r = pi[d];
+      uint2 w;
+      if (ll_ready(v[d], epoch)) {
+        w = make_uint2(v[d].x, v[d].z);
+      } else {
+        int e = 0;
+        if (!poll_ll(ll_slot(S.pad[rank], par, r) + kLLHeader + ui[d] * 16, epoch, S.pad[rank],
+                     c.timeout_ns, w, &e)) {
+          atomicCAS(&s_err, 0, e);
+          break;
+        }
+      }
+      store8(a.rptr[r], ui[d], a.rbytes[r], w);
+    }
+  }
+  __syncthreads();
+  if (s_err && tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
 }
 
 __global__ void __launch_bounds__(kLLThreads) k_exchange_ll(DevComm c, LLArgs a) {
