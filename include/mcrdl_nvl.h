@@ -159,6 +159,14 @@ mcrdl_status_t mcrdl_all_reduce(mcrdl_comm* comm, const void* in, void* out, uin
                                 mcrdl_dtype_t dtype, mcrdl_redop_t op, mcrdl_algo_t algo,
                                 uint64_t seq, void* stream);
 
+/* reduce (runtime.py:519-526; oracle reference.py:27-33): the two-shot
+ * pipeline in root mode — every rank's reduced segment goes to the root only
+ * (ascending fold, bit-exact). `out` is written on the root only and may be
+ * NULL elsewhere. */
+mcrdl_status_t mcrdl_reduce(mcrdl_comm* comm, const void* in, void* out, uint64_t count,
+                            mcrdl_dtype_t dtype, mcrdl_redop_t op, int root, mcrdl_algo_t algo,
+                            uint64_t seq, void* stream);
+
 /* reduce_scatter (runtime.py:590-597; collectives.py:609-645; oracle
  * reference.py:79-83): in holds world*recvcount elements, rank r receives the
  * ascending-fold reduction of segment r. Needs 16-byte aligned buffers and

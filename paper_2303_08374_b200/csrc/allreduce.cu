@@ -249,7 +249,8 @@ __device__ __forceinline__ void tma_drain() {
 template <typename T, int OP, bool VEC, bool TMA>
 __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int64_t n, int64_t sp,
                                              int64_t segb, int gp, int gs, int64_t chp, int ag_pull,
-                                             uint32_t epoch, uint32_t sig, T* rs_out, int64_t rs_n) {
+                                             int root, uint32_t epoch, uint32_t sig, T* rs_out,
+                                             int64_t rs_n) {
   constexpr int N = Pack<T>::N;
   __shared__ int s_err;
   __shared__ SComm S;
@@ -387,6 +388,13 @@ __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int
             store_pack<T, VEC>(rs_out, i, rs_n, res);
             continue;
           }
+          if (root >= 0) {  // reduce: the segment goes to the root only
+            if (rank == root)
+              store_pack<T, VEC>(out, int64_t(rank) * sp + i, n, res);
+            else
+              st16(S.ws[root] + hoff + ag + int64_t(rank) * segb + i * 16, res);
+            continue;
+          }
           if (ag_pull) {  // peers pull it from my workspace
             st16(S.ws[rank] + hoff + ag + int64_t(rank) * segb + i * 16, res);
           } else {
@@ -400,7 +408,7 @@ __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int
       }
       if (rs_out != nullptr) continue;
       __syncthreads();
-      if (tid < world && tid != rank)
+      if (tid < world && tid != rank && (root < 0 || tid == root))
         publish(&S.pad[tid]->flag2[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
       MCRDL_TRACE_AT(c, bid, 2 + 2 * r);
     }
@@ -410,6 +418,7 @@ __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int
 
   // ------------------------------------------------------------- gatherer
   if (rs_out != nullptr) return;  // reduce_scatter has no all-gather phase
+  if (root >= 0 && rank != root) return;  // reduce: only the root gathers
   int rows = 0;
   for (int q = 0; q < world; ++q)
     if (q != rank) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
@@ -462,10 +471,11 @@ __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int
 template <typename T, int OP, bool VEC, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2)
     k_ar_pipe(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp, int gs,
-              int64_t chp, int ag_pull, uint32_t sig, T* rs_out = nullptr, int64_t rs_n = 0) {
+              int64_t chp, int ag_pull, int root, uint32_t sig, T* rs_out = nullptr,
+              int64_t rs_n = 0) {
   const uint32_t epoch = epoch_enter(c);
-  ar_pipe_body<T, OP, VEC, TMA>(c, in, out, n, sp, segb, gp, gs, chp, ag_pull, epoch, sig, rs_out,
-                                rs_n);
+  ar_pipe_body<T, OP, VEC, TMA>(c, in, out, n, sp, segb, gp, gs, chp, ag_pull, root, epoch, sig,
+                                rs_out, rs_n);
   epoch_exit(c, epoch);
 }
 
@@ -1285,15 +1295,17 @@ static bool try_ar_symm(mcrdl_comm* c, const T* in, T* out, int64_t n, mcrdl_alg
 
 template <typename T, int OP>
 static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mcrdl_algo_t algo,
-                               uint64_t seq, int dt, cudaStream_t stream) {
+                               uint64_t seq, int dt, cudaStream_t stream, int root = -1) {
   constexpr int N = Pack<T>::N;
   const int world = c->world;
   const int64_t half = c->dc.half_bytes;
   const bool vec = ((uintptr_t(in) | uintptr_t(out)) & 15) == 0;
   if (world == 1) return launch_local_copy(out, in, n * int64_t(sizeof(T)), c->num_sms, stream);
-  {
+  if (root < 0) {
     mcrdl_status_t sst;
     if (try_ar_symm<T, OP>(c, in, out, n, algo, seq, dt, stream, &sst)) return sst;
+  } else {
+    algo = MCRDL_ALGO_TWO_SHOT;  // reduce: RS + gather to the root (k_ar_pipe root mode)
   }
   const int64_t bytes = n * int64_t(sizeof(T));
   const int64_t oneshot_max = half / world / 256 * 256;
@@ -1324,7 +1336,10 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
     const int64_t m = (n - done < chunk_elems) ? (n - done) : chunk_elems;
     mcrdl_status_t st = begin_op(c, stream);
     if (st != MCRDL_OK) return st;
-    const uint32_t sig = op_sig(kKindAllReduce, dt, OP, sub, uint64_t(m), seq);
+    const uint32_t sig =
+        root < 0 ? op_sig(kKindAllReduce, dt, OP, sub, uint64_t(m), seq)
+                 : mix32(op_sig(kKindReduce, dt, OP, sub, uint64_t(m), seq), uint64_t(root)) &
+                       ~kSigCodecBit;
     const T* ip = in + done;
     T* op = out + done;
     const int64_t npk = (m + N - 1) / N;
@@ -1410,7 +1425,7 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
         const int64_t sharew = (sp + gw - 1) / gw;
         int64_t chpw = (sharew + 3999) / 4000;
         if (chpw < chunk_kb * 64) chpw = chunk_kb * 64;
-        if (ws_kernel == 1) {
+        if (ws_kernel == 1 && root < 0) {
           if (vec)
             k_ar_ws<T, OP, true><<<int(gw), kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, chpw,
                                                                    sig);
@@ -1429,13 +1444,13 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
           int64_t chpt = (sharet + 3999) / 4000;
           if (chpt < chunk_kb * 64) chpt = chunk_kb * 64;
           k_ar_pipe<T, OP, true, true><<<int(gs + 2 * gpt), kThreads, 0, stream>>>(
-              c->dc, ip, op, m, sp, segb, int(gpt), gs, chpt, ag_pull, sig);
+              c->dc, ip, op, m, sp, segb, int(gpt), gs, chpt, ag_pull, root, sig);
         } else if (vec) {
           k_ar_pipe<T, OP, true, false><<<G, kThreads, 0, stream>>>(
-              c->dc, ip, op, m, sp, segb, int(gp), int(gp), chp, ag_pull, sig);
+              c->dc, ip, op, m, sp, segb, int(gp), int(gp), chp, ag_pull, root, sig);
         } else {
           k_ar_pipe<T, OP, false, false><<<G, kThreads, 0, stream>>>(
-              c->dc, ip, op, m, sp, segb, int(gp), int(gp), chp, ag_pull, sig);
+              c->dc, ip, op, m, sp, segb, int(gp), int(gp), chp, ag_pull, root, sig);
         }
       }
     }
@@ -1449,14 +1464,15 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
 
 template <typename T>
 static mcrdl_status_t ar_op(mcrdl_comm* c, const void* in, void* out, int64_t n, mcrdl_redop_t op,
-                            mcrdl_algo_t algo, uint64_t seq, int dt, cudaStream_t s) {
+                            mcrdl_algo_t algo, uint64_t seq, int dt, cudaStream_t s,
+                            int root = -1) {
   const T* i = reinterpret_cast<const T*>(in);
   T* o = reinterpret_cast<T*>(out);
   switch (op) {
-    case MCRDL_SUM: return ar_typed<T, MCRDL_SUM>(c, i, o, n, algo, seq, dt, s);
-    case MCRDL_PROD: return ar_typed<T, MCRDL_PROD>(c, i, o, n, algo, seq, dt, s);
-    case MCRDL_MIN: return ar_typed<T, MCRDL_MIN>(c, i, o, n, algo, seq, dt, s);
-    case MCRDL_MAX: return ar_typed<T, MCRDL_MAX>(c, i, o, n, algo, seq, dt, s);
+    case MCRDL_SUM: return ar_typed<T, MCRDL_SUM>(c, i, o, n, algo, seq, dt, s, root);
+    case MCRDL_PROD: return ar_typed<T, MCRDL_PROD>(c, i, o, n, algo, seq, dt, s, root);
+    case MCRDL_MIN: return ar_typed<T, MCRDL_MIN>(c, i, o, n, algo, seq, dt, s, root);
+    case MCRDL_MAX: return ar_typed<T, MCRDL_MAX>(c, i, o, n, algo, seq, dt, s, root);
   }
   return set_error(MCRDL_ERR_VALIDATION, "unknown reduce op %d", int(op));
 }
@@ -1487,7 +1503,7 @@ static mcrdl_status_t rs_typed(mcrdl_comm* c, const T* in, T* out, int64_t m, ui
   if (chp < 16384) chp = 16384;
   // senders + reducers only (reduce_scatter has no all-gather role)
   k_ar_pipe<T, OP, true, false><<<int(2 * gp), kThreads, 0, stream>>>(
-      c->dc, in, out, int64_t(world) * m, sp, segb, int(gp), int(gp), chp, 0, sig, out, m);
+      c->dc, in, out, int64_t(world) * m, sp, segb, int(gp), int(gp), chp, 0, -1, sig, out, m);
   count_launch();
   MCRDL_CUDA_CHECK(cudaGetLastError());
   return MCRDL_OK;
@@ -1563,6 +1579,35 @@ mcrdl_status_t mcrdl_all_reduce(mcrdl_comm* c, const void* in, void* out, uint64
     case MCRDL_I64: return ar_op<int64_t>(c, in, out, n, op, algo, seq, int(dtype), s);
     case MCRDL_U8: return ar_op<uint8_t>(c, in, out, n, op, algo, seq, int(dtype), s);
     case MCRDL_BF16: return ar_op<__nv_bfloat16>(c, in, out, n, op, algo, seq, int(dtype), s);
+  }
+  return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+}
+
+// reduce (runtime.py:519-526; collectives.py _reduce_linear/_binomial; oracle
+// reference.py:27-33): the two-shot pipeline in root mode — reduce-scatter as
+// for all_reduce, then every rank sends its reduced segment to the root only
+// (non-roots move (p-1)/p·S + S/p instead of 2(p-1)/p·S; only the root's
+// gatherers run). Ascending fold: bit-exact. out may be NULL off the root.
+mcrdl_status_t mcrdl_reduce(mcrdl_comm* c, const void* in, void* out, uint64_t count,
+                            mcrdl_dtype_t dtype, mcrdl_redop_t op, int root, mcrdl_algo_t algo,
+                            uint64_t seq, void* stream) {
+  (void)algo;
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  if (root < 0 || root >= c->world)
+    return set_error(MCRDL_ERR_VALIDATION, "root %d outside world %d", root, c->world);
+  if (count == 0) return mcrdl_barrier(c, seq, stream);
+  if (in == nullptr || (out == nullptr && c->rank == root))
+    return set_error(MCRDL_ERR_VALIDATION, "NULL buffer");
+  if (out == nullptr) out = const_cast<void*>(in);  // never written off the root
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t n = int64_t(count);
+  switch (dtype) {
+    case MCRDL_F32: return ar_op<float>(c, in, out, n, op, algo, seq, int(dtype), s, root);
+    case MCRDL_F64: return ar_op<double>(c, in, out, n, op, algo, seq, int(dtype), s, root);
+    case MCRDL_I32: return ar_op<int32_t>(c, in, out, n, op, algo, seq, int(dtype), s, root);
+    case MCRDL_I64: return ar_op<int64_t>(c, in, out, n, op, algo, seq, int(dtype), s, root);
+    case MCRDL_U8: return ar_op<uint8_t>(c, in, out, n, op, algo, seq, int(dtype), s, root);
+    case MCRDL_BF16: return ar_op<__nv_bfloat16>(c, in, out, n, op, algo, seq, int(dtype), s, root);
   }
   return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
 }

@@ -134,6 +134,7 @@ inline uint32_t op_sig(int kind, int dtype, int op, int root, uint64_t count, ui
 // Kind tags folded into signatures (CommOpKind order, core.py:89-104).
 enum KindTag : int {
   kKindBcast = 2,
+  kKindReduce = 3,
   kKindAllReduce = 4,
   kKindGatherv = 6,
   kKindAllGatherv = 10,

@@ -44,6 +44,7 @@ SIGNATURES = {
     "mcrdl_symm_free": (c_int, [_P, _P]),
     "mcrdl_all_reduce": (c_int, [_P, _P, _P, c_uint64, c_int, c_int, c_int, c_uint64, _P]),
     "mcrdl_reduce_scatter": (c_int, [_P, _P, _P, c_uint64, c_int, c_int, c_int, c_uint64, _P]),
+    "mcrdl_reduce": (c_int, [_P, _P, _P, c_uint64, c_int, c_int, c_int, c_int, c_uint64, _P]),
     "mcrdl_all_to_allv": (c_int, [_P, _P, _P, _I64P, _I64P, _I64P, _I64P, c_int, c_int, c_uint64, _P]),
     "mcrdl_all_to_allv_dev": (c_int, [_P, _P, c_uint64, _P, c_uint64, _P, c_int, c_int, c_uint64,
                                       _P]),

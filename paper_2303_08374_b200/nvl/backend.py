@@ -613,12 +613,19 @@ class NvlBackendInstance:
                 chk(lib.mcrdl_all_reduce(c, _ptr(i), _ptr(o), req.input.count, dt.code, op, algo,
                                          seq, s))
             elif kind is CommOpKind.reduce:
-                if rank == req.root:
-                    o = st.dev(req.output, upload=req.output is req.input, download=True)
+                o = (st.dev(req.output, upload=req.output is req.input, download=True)
+                     if rank == req.root else None)
+                # native root mode of the two-shot pipeline where all_reduce would
+                # run two-shot anyway; small messages: one-shot / LL all_reduce
+                big = req.input.nbytes > ((8 << 20) if p == 2 else (2 << 20))
+                if p > 1 and (big or name == "two_shot"):
+                    chk(lib.mcrdl_reduce(c, _ptr(i), _ptr(o) if o is not None else None,
+                                         req.input.count, dt.code, op, req.root, algo, seq, s))
                 else:
-                    o = st.scratch(req.input.count, dt)
-                chk(lib.mcrdl_all_reduce(c, _ptr(i), _ptr(o), req.input.count, dt.code, op, algo,
-                                         seq, s))
+                    if o is None:
+                        o = st.scratch(req.input.count, dt)
+                    chk(lib.mcrdl_all_reduce(c, _ptr(i), _ptr(o), req.input.count, dt.code, op,
+                                             algo, seq, s))
             else:
                 m = req.output.count
                 o = st.dev(req.output, upload=False, download=True)

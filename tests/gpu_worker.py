@@ -346,6 +346,35 @@ def sc_reduce_family(cx: Ctx):
             cx.check(f"reduce/root{root}", from_dev(t, DType.f32), seqref.fold(ins, "sum"))
         else:
             cx.check(f"reduce/nonroot-untouched/{root}", from_dev(t, DType.f32), ins[r])
+    # native root mode (mcrdl_reduce: RS + gather to the root): large messages
+    # and explicit two_shot, every dtype/op, in place and out of place,
+    # misaligned, multi-chunk; non-roots untouched
+    inst = cx.rt._instance(cx.b)
+    cases = [(DType.f32, "sum", (3 << 20) + 5, "auto"), (DType.bf16, "sum", 5 << 20, "auto"),
+             (DType.i64, "max", 40_001, "two_shot"), (DType.i32, "min", 99_999, "two_shot"),
+             (DType.u8, "sum", 3_000_003, "auto"), (DType.f64, "prod", 4097, "two_shot"),
+             (DType.f32, "sum", (160 << 20) // 4 + 3, "auto")]
+    for dtype, op, n, algo in cases:
+        inst.policy = AlgorithmPolicy({CommOpKind.reduce: algo})
+        root = (n + 1) % p
+        gen = small_prod_values if op == "prod" else values
+        ins = [gen(dtype, n, "rednat", dtype.name, op, n, q) for q in range(p)]
+        want = (seqref.fold_bf16 if dtype is DType.bf16 else seqref.fold)(ins, op)
+        src = to_dev(ins[r], dtype, cx.dev)
+        if n % 2:  # out of place into a misaligned view (every rank passes one,
+            # as the reference's validate requires; only the root's is written)
+            out = torch.zeros(n + 1, dtype=src.dtype, device=cx.dev)[1:]
+            cx.rt.post(CommRequest(CommOpKind.reduce, input=Buffer(src), output=Buffer(out),
+                                   root=root, op=ReduceOp(op), backend=cx.b))
+            got = out if r == root else None
+        else:
+            cx.rt.reduce(cx.b, Buffer(src), root, ReduceOp(op))
+            got = src
+        if r == root:
+            cx.check(f"reduce/native/{dtype.name}/{op}/{n}", from_dev(got, dtype), want)
+        elif got is not None:
+            cx.check(f"reduce/native-untouched/{dtype.name}/{n}", from_dev(got, dtype), ins[r])
+    inst.policy = AlgorithmPolicy()
     # composed path (m*8 % 16 != 0) and the native RS kernel (aligned segments)
     for dtype, m, op in ((DType.i64, 1001, "sum"), (DType.f32, 1 << 16, "sum"),
                          (DType.bf16, 4096, "sum"), (DType.i32, 12288, "max"),
