@@ -1315,6 +1315,13 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
     const int64_t thr = world == 2 ? (int64_t(8) << 20) : world <= 4 ? (int64_t(2) << 20)
                                                                       : (int64_t(1) << 20);
     algo = bytes <= thr ? MCRDL_ALGO_ONE_SHOT : MCRDL_ALGO_TWO_SHOT;
+    // NVLS for large f32/bf16 sums: its link traffic is (1 + 1/p)·S against
+    // 2(p-1)/p·S for two-shot. Measured at p = 4 (profiles/nvls_vs_twoshot_r1_p4.csv,
+    // full_sweep_r1_p4.csv): ahead from ~256 MiB (582-592 vs 540-572 GB/s),
+    // behind at 64 MiB; at p >= 6 the traffic ratio (1.125 vs 1.75 at p = 8)
+    // moves the crossover down, taken here as 16 MiB.
+    const int64_t nvls_thr = world >= 6 ? (int64_t(16) << 20) : (int64_t(128) << 20);
+    if (world >= 4 && bytes >= nvls_thr) algo = MCRDL_ALGO_NVLS;
   }
   // NVLS: the switch reduces; sum of f32/bf16 only, and only when every rank
   // built the multicast object (caps.nvls_supported). Otherwise two-shot.
