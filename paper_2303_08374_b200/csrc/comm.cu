@@ -646,7 +646,8 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   int64_t mbox = int64_t(env_int("MCRDL_P2P_BYTES", int64_t(kP2PSlots) * kP2PChunk));
   mbox = std::min<int64_t>(mbox, int64_t(kP2PSlots) * kP2PChunk) / kP2PChunk * kP2PChunk;
   if (mbox < 0) mbox = 0;
-  const uint64_t p2p_bytes = uint64_t(mbox) * uint64_t(world);
+  const uint64_t p2p_bytes =
+      (uint64_t(mbox) + (mbox > 0 ? uint64_t(kP2PLLSenderBytes) : 0)) * uint64_t(world);
   if ((st = alloc_region(c, kPadBytes + workspace_bytes + p2p_bytes, &c->base)) != MCRDL_OK)
     return fail(st);
   MCRDL_CUDA_CHECK(cudaMemset(reinterpret_cast<void*>(c->base.ptr[rank]), 0, kPadBytes));

@@ -27,7 +27,7 @@
 // or before the send when a rank both sends and receives large messages.
 #include <algorithm>
 
-#include "internal.h"
+#include "ll.cuh"
 
 namespace mcrdl {
 
@@ -39,11 +39,145 @@ __device__ __forceinline__ uint8_t* mailbox(const DevComm& c, uint8_t* ws_owner,
   return ws_owner + 2 * c.half_bytes + int64_t(sender) * c.mbox_bytes;
 }
 
+// LL ring of `sender` in the mailbox area of the rank owning `ws_owner`
+// (after the bulk mailboxes).
+__device__ __forceinline__ uint8_t* ll_box(const DevComm& c, uint8_t* ws_owner, int sender) {
+  return ws_owner + 2 * c.half_bytes + int64_t(c.world) * c.mbox_bytes +
+         int64_t(sender) * kP2PLLSenderBytes;
+}
+
+// Receiver side: wait for message `msg` from `peer` on EITHER path and report
+// which one the sender took (a byte-count disagreement can make the two ends
+// choose different paths: that is a LengthMismatch, not a hang).
+static __device__ __noinline__ int p2p_wait_header(const DevComm& c, const Pad* me, int peer,
+                                                   const uint8_t* ll_hdr, uint64_t msg,
+                                                   bool* via_ll, uint64_t* bytes) {
+  const uint64_t* h = me->p2p_hdr[peer][msg % kP2PHdr];
+  const uint32_t tag = uint32_t(msg + 1);
+  uint64_t start = 0;
+  for (int spins = 0;; ++spins) {
+    if (ld_acquire_sys(&h[0]) >= msg + 1) {
+      if (ld_relaxed_sys(&h[0]) != msg + 1) return MCRDL_ERR_ORDER_MISMATCH;  // lapped
+      *via_ll = false;
+      *bytes = ld_relaxed_sys(&h[1]);
+      return MCRDL_OK;
+    }
+    const uint4 v = ld_ll(ll_hdr);
+    if (ll_ready(v, tag)) {
+      *via_ll = true;
+      *bytes = uint64_t(v.x) | (uint64_t(v.z) << 32);
+      return MCRDL_OK;
+    }
+    if (spins >= 32) {
+      spins = 0;
+      if (const uint64_t pz = ld_relaxed_sys(&me->poison)) return int(pz);
+      const uint64_t now = globaltimer_ns();
+      if (start == 0) start = now;
+      else if (now - start > c.timeout_ns) return MCRDL_ERR_TIMEOUT;
+    }
+  }
+}
+
+__device__ __forceinline__ bool last_cta(const DevComm& c, int dir);
+
+// ------------------------------------------------------------ LL messages
+// One CTA. Sender: wait until the receiver matched message msg - kP2PLLSlots
+// (p2p_hdr_ack counts every message, LL or bulk), then write the payload as
+// {d0, tag, d1, tag} lines and the header line {bytes, tag} — no fences, no
+// flags. Receiver: poll the header line, then the data lines themselves.
+__global__ void __launch_bounds__(kP2PThreads)
+    k_send_ll(DevComm c, uint8_t* peer_ws, const uint8_t* buf, int64_t bytes, int peer) {
+  __shared__ uint64_t s_msg;
+  __shared__ int s_err;
+  Pad* me = c.self;
+  oplog_start(c);
+  if (threadIdx.x == 0) {
+    const uint64_t msg = *reinterpret_cast<volatile uint64_t*>(&me->p2p_tx_msgs[peer]);
+    s_msg = msg;
+    s_err = msg >= uint64_t(kP2PLLSlots)
+                ? wait_geq(&me->p2p_hdr_ack[peer], me, c.timeout_ns, msg + 1 - kP2PLLSlots)
+                : MCRDL_OK;
+  }
+  __syncthreads();
+  const uint64_t msg = s_msg;
+  if (s_err) {
+    if (threadIdx.x == 0) raise_error(const_cast<Pad* const*>(c.pad), c.world, c.err, s_err, 0);
+  } else {
+    uint8_t* slot = ll_box(c, peer_ws, c.rank) + int64_t(msg % kP2PLLSlots) * kP2PLLSlotBytes;
+    const uint32_t tag = uint32_t(msg + 1);
+    const int64_t nu = (bytes + 7) / 8;
+    const int64_t u0 = nu * blockIdx.x / gridDim.x, u1 = nu * (blockIdx.x + 1) / gridDim.x;
+    for (int64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+      const uint2 v = load8(buf, u, bytes);
+      st_ll(slot + 16 + u * 16, v.x, v.y, tag);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      st_ll(slot, uint32_t(bytes), uint32_t(uint64_t(bytes) >> 32), tag);
+  }
+  if (last_cta(c, 0)) {
+    me->p2p_tx_msgs[peer] = msg + 1;
+    oplog_end(c);
+  }
+}
+
+__global__ void __launch_bounds__(kP2PThreads)
+    k_recv_ll(DevComm c, Pad* peer_pad, uint8_t* my_ws, uint8_t* buf, int64_t bytes, int peer) {
+  __shared__ uint64_t s_msg;
+  __shared__ int s_err;
+  Pad* me = c.self;
+  oplog_start(c);
+  const uint8_t* base = ll_box(c, my_ws, peer);
+  if (threadIdx.x == 0) {
+    const uint64_t msg = *reinterpret_cast<volatile uint64_t*>(&me->p2p_rx_msgs[peer]);
+    s_msg = msg;
+    int e = MCRDL_OK;
+    if (blockIdx.x == 0) {  // CTA 0 matches the header; the others poll data lines
+      bool via_ll = false;
+      uint64_t sent = 0;
+      e = p2p_wait_header(c, me, peer, base + int64_t(msg % kP2PLLSlots) * kP2PLLSlotBytes, msg,
+                          &via_ll, &sent);
+      if (e == MCRDL_OK && (!via_ll || sent != uint64_t(bytes))) e = MCRDL_ERR_LENGTH_MISMATCH;
+      if (e) raise_error(const_cast<Pad* const*>(c.pad), c.world, c.err, e, 0);
+    }
+    s_err = e;
+  }
+  __syncthreads();
+  const uint64_t msg = s_msg;
+  const uint8_t* slot = base + int64_t(msg % kP2PLLSlots) * kP2PLLSlotBytes;
+  const uint32_t tag = uint32_t(msg + 1);
+  const int64_t nu = (bytes + 7) / 8;
+  const int64_t u0 = nu * blockIdx.x / gridDim.x, u1 = nu * (blockIdx.x + 1) / gridDim.x;
+  volatile int* verr = &s_err;
+  for (int64_t u = u0 + threadIdx.x; u < u1 && !*verr; u += blockDim.x) {
+    uint2 d;
+    const uint4 v = ld_ll(slot + 16 + u * 16);
+    if (ll_ready(v, tag)) {
+      d = make_uint2(v.x, v.z);
+    } else {
+      int e = 0;
+      if (!poll_ll(slot + 16 + u * 16, tag, me, c.timeout_ns, d, &e)) {
+        atomicCAS(&s_err, 0, e);
+        break;
+      }
+    }
+    store8(buf, u, bytes, d);
+  }
+  __syncthreads();
+  if (s_err && threadIdx.x == 0 && blockIdx.x != 0)
+    raise_error(const_cast<Pad* const*>(c.pad), c.world, c.err, s_err, 0);
+  if (last_cta(c, 1)) {
+    publish(&peer_pad->p2p_hdr_ack[c.rank], msg + 1);  // slot consumed
+    me->p2p_rx_msgs[peer] = msg + 1;
+    oplog_end(c);
+  }
+}
+
 // Last CTA of the launch advances the local stream counters. Sends and
 // receives have their own exit counters (and order chains, begin_op): a recv
 // may run concurrently with a send or a collective on another stream.
 __device__ __forceinline__ bool last_cta(const DevComm& c, int dir) {
   __syncthreads();
+  if (gridDim.x == 1) return threadIdx.x == 0;  // single CTA: no exit counter
   bool last = false;
   if (threadIdx.x == 0) {
     __threadfence();
@@ -58,7 +192,7 @@ __device__ __forceinline__ bool last_cta(const DevComm& c, int dir) {
 
 __global__ void __launch_bounds__(kP2PThreads)
     k_send(DevComm c, Pad* peer_pad, uint8_t* peer_ws, const uint8_t* buf, int64_t bytes, int peer,
-           int K) {
+           int K, int64_t chunk) {
   __shared__ uint64_t s_base, s_msg;
   __shared__ int s_err;
   Pad* me = c.self;
@@ -70,7 +204,7 @@ __global__ void __launch_bounds__(kP2PThreads)
   }
   __syncthreads();
   const uint64_t base = s_base, msg = s_msg;
-  const int64_t nch = (bytes + kP2PChunk - 1) / kP2PChunk;
+  const int64_t nch = (bytes + chunk - 1) / chunk;  // chunk <= slot size
   const int rank = c.rank;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // header slot msg % H is free once the receiver matched message msg - H
@@ -97,8 +231,8 @@ __global__ void __launch_bounds__(kP2PThreads)
     }
     __syncthreads();
     if (s_err) break;
-    const int64_t off = k * kP2PChunk;
-    block_copy<8>(box + int64_t(slot) * kP2PChunk, buf + off, min(kP2PChunk, bytes - off));
+    const int64_t off = k * chunk;
+    block_copy<8>(box + int64_t(slot) * kP2PChunk, buf + off, min(chunk, bytes - off));
     __syncthreads();
     if (threadIdx.x == 0) publish(&peer_pad->p2p_full[rank][slot], g + 1);
   }
@@ -114,7 +248,7 @@ __global__ void __launch_bounds__(kP2PThreads)
 
 __global__ void __launch_bounds__(kP2PThreads)
     k_recv(DevComm c, Pad* peer_pad, const uint8_t* my_ws, uint8_t* buf, int64_t bytes, int peer,
-           int K) {
+           int K, int64_t chunk) {
   __shared__ uint64_t s_base, s_msg;
   __shared__ int s_err;
   Pad* me = c.self;
@@ -126,15 +260,17 @@ __global__ void __launch_bounds__(kP2PThreads)
   }
   __syncthreads();
   const uint64_t base = s_base, msg = s_msg;
-  const int64_t nch = (bytes + kP2PChunk - 1) / kP2PChunk;
+  const int64_t nch = (bytes + chunk - 1) / chunk;  // chunk <= slot size
   const int rank = c.rank;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint64_t* h = me->p2p_hdr[peer][msg % kP2PHdr];
-    int e = wait_geq(&h[0], me, c.timeout_ns, msg + 1);
+    bool via_ll = false;
+    uint64_t sent = 0;
+    int e = p2p_wait_header(c, me, peer,
+                            ll_box(c, const_cast<uint8_t*>(my_ws), peer) +
+                                int64_t(msg % kP2PLLSlots) * kP2PLLSlotBytes,
+                            msg, &via_ll, &sent);
     if (e == MCRDL_OK) {
-      const uint64_t sent = ld_relaxed_sys(&h[1]);
-      if (ld_relaxed_sys(&h[0]) != msg + 1) e = MCRDL_ERR_ORDER_MISMATCH;  // lapped
-      else if (sent != uint64_t(bytes)) e = MCRDL_ERR_LENGTH_MISMATCH;
+      if (via_ll || sent != uint64_t(bytes)) e = MCRDL_ERR_LENGTH_MISMATCH;
       else publish(&peer_pad->p2p_hdr_ack[rank], msg + 1);
     }
     s_err = e;
@@ -152,8 +288,8 @@ __global__ void __launch_bounds__(kP2PThreads)
     }
     __syncthreads();
     if (s_err) break;
-    const int64_t off = k * kP2PChunk;
-    block_copy<8>(buf + off, box + int64_t(slot) * kP2PChunk, min(kP2PChunk, bytes - off));
+    const int64_t off = k * chunk;
+    block_copy<8>(buf + off, box + int64_t(slot) * kP2PChunk, min(chunk, bytes - off));
     __syncthreads();
     if (threadIdx.x == 0) publish(&peer_pad->p2p_free[rank][slot], g + 1);
   }
@@ -179,17 +315,35 @@ mcrdl_status_t p2p_launch(mcrdl_comm* c, void* buf, uint64_t bytes, int peer, bo
   mcrdl_status_t st = begin_op(c, stream, is_send ? kChainSend : kChainRecv);
   if (st != MCRDL_OK) return st;
   const int K = int(c->dc.mbox_bytes / kP2PChunk);
-  const int64_t nch = int64_t((bytes + kP2PChunk - 1) / kP2PChunk);
+  // Chunk = one 64 KiB slot. (Smaller chunks to spread medium messages over
+  // more CTAs measured slower: 256 KiB ping-pong 43 vs 37 us with 4 KiB chunks;
+  // the per-chunk flag round trips dominate.)
+  const int64_t chunk = kP2PChunk;
+  const int64_t nch = (int64_t(bytes) + chunk - 1) / chunk;
   // one CTA per chunk in flight, at most the ring depth and one per SM
   int G = int(std::min<int64_t>(std::max<int64_t>(nch, 1), std::min(K, c->num_sms)));
   if (G < 1) G = 1;
   Pad* peer_pad = c->dc.pad[peer];
+  if (bytes <= uint64_t(kP2PLLMax)) {  // small: LL lines, 8 KiB of payload per CTA
+    const int gl = int(std::max<uint64_t>(1, (bytes + kP2PLLCtaBytes - 1) / kP2PLLCtaBytes));
+    if (is_send)
+      k_send_ll<<<gl, kP2PThreads, 0, stream>>>(c->dc, c->dc.ws[peer],
+                                                static_cast<const uint8_t*>(buf), int64_t(bytes),
+                                                peer);
+    else
+      k_recv_ll<<<gl, kP2PThreads, 0, stream>>>(c->dc, peer_pad, c->dc.ws[c->rank],
+                                                static_cast<uint8_t*>(buf), int64_t(bytes), peer);
+    count_launch();
+    MCRDL_CUDA_CHECK(cudaGetLastError());
+    return MCRDL_OK;
+  }
   if (is_send) {
     k_send<<<G, kP2PThreads, 0, stream>>>(c->dc, peer_pad, c->dc.ws[peer],
-                                          static_cast<const uint8_t*>(buf), int64_t(bytes), peer, K);
+                                          static_cast<const uint8_t*>(buf), int64_t(bytes), peer, K,
+                                          chunk);
   } else {
     k_recv<<<G, kP2PThreads, 0, stream>>>(c->dc, peer_pad, c->dc.ws[c->rank], static_cast<uint8_t*>(buf),
-                                          int64_t(bytes), peer, K);
+                                          int64_t(bytes), peer, K, chunk);
   }
   count_launch();
   MCRDL_CUDA_CHECK(cudaGetLastError());
