@@ -261,6 +261,8 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
   }
 
   const int me = tid;  // peer index this thread handles in flag duties (tid < world)
+  const int bid = int(blockIdx.x);
+  MCRDL_TRACE_AT(c, bid, 0);
   if (sender) {
     if (s == 0 && !a.codec)
       exchange_ll_send_pairs(S.pad, rank, world, par, s_sp, s_sb, a.sig_base, epoch);
@@ -297,17 +299,21 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
           publish(&S.pad[me]->flag[par][s][rank],
                   make_flag(epoch, pair_sig(a.sig_base, s_sb[me]), uint32_t(sent)));
         }
+        MCRDL_TRACE_AT(c, bid, 1 + r);
       }
     }
+    MCRDL_TRACE_AT(c, bid, kTraceSlots - 1);
     return;
   }
 
   // ------------------------------------------------------------- receiver
-  {  // local segment: straight copy (skipped when in place)
+  {  // local segment: straight copy (skipped when in place). (Interleaving it
+     // with the row-flag waits measured neutral: tools/trace_x.py.)
     int64_t lo, hi;
     byte_share(s_sb[rank], s, a.gp, lo, hi);
     block_copy<4>(s_rp[rank] + lo, s_sp[rank] + lo, hi - lo);
   }
+  MCRDL_TRACE_AT(c, bid, 1);
   if (s == 0 && !a.codec) {
     const int e = exchange_ll_recv_pairs(S.pad, rank, world, par, s_rp, s_rb, a.sig_base, epoch,
                                          c.timeout_ns);
@@ -334,6 +340,7 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
         ++got;
       }
       __syncthreads();
+      MCRDL_TRACE_AT(c, bid, 2 + 2 * r);
       if (s_err) {
         if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
         return;
@@ -347,6 +354,7 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
         else
           block_copy<4>(s_rp[i] + t * slot + lo, my_ws + int64_t(i) * slot + lo, hi - lo);
       }
+      MCRDL_TRACE_AT(c, bid, 3 + 2 * r);
     }
     // Round t of every pair fully landed: let senders reuse the slot.
     if (G.more) {
@@ -356,6 +364,7 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
                 make_flag(epoch, pair_sig(a.sig_base, s_rb[me]), uint32_t(t + 1)));
     }
   }
+  MCRDL_TRACE_AT(c, bid, kTraceSlots - 1);
 }
 
 __global__ void __launch_bounds__(kThreads, 2) k_exchange(DevComm c, XArgs a) {
