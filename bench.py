@@ -244,7 +244,14 @@ def run_native(args) -> int:
     clocks = ClockSampler(local)
     clocks.start()
     rt = Runtime(rank, world)
-    rt.init([BackendConfig("nvl", workspace_bytes=2 << 30)])
+    cfgs = [BackendConfig("nvl", workspace_bytes=2 << 30)]
+    if world > 1 and not args.no_secondary:
+        # cfg5's fused small-tensor all_reduces (FusionConfig B = 1 MiB, T = 5 ms)
+        from paper_2303_08374_b200 import FusionConfig
+
+        cfgs.append(BackendConfig("nvl_fused", workspace_bytes=256 << 20,
+                                  fusion=FusionConfig(max_bytes=1 << 20, max_wait=0.005)))
+    rt.init(cfgs)
     size = args.size_mib * MIB
     n = size // 4
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -484,6 +491,77 @@ def secondary(rt, world, rank, dev, size, barrier, max_over_ranks):
         except Exception as exc:  # noqa: BLE001
             res["nccl_error"] = repr(exc)
     out["all_to_allv_dlrm"] = res
+
+    # DLRM cfg4, skewed variant: per-rank batch b_j from Zipf(1.1) weights
+    # (w_j = (j+1)^-1.1, normalized to 65536, remainder to the last rank)
+    wz = [(j + 1) ** -1.1 for j in range(world)]
+    bz = [int(B * w / sum(wz)) for w in wz]
+    bz[-1] += B - sum(bz)
+    ssc = [bz[j] * tables[rank] * 128 for j in range(world)]
+    src = [bz[rank] * tables[j] * 128 for j in range(world)]
+    ssd = [sum(ssc[:j]) for j in range(world)]
+    srd = [sum(src[:j]) for j in range(world)]
+    sinp = torch.randn(sum(ssc), device=dev)
+    sout = torch.empty(sum(src), device=dev)
+    SI, SO = Buffer(sinp), Buffer(sout)
+    t = dev_time(lambda: rt.all_to_allv("nvl", SO, SI, ssc, src, ssd, srd))
+    egress = max_over_ranks(max(sum(ssc) - ssc[rank], sum(src) - src[rank]) * 4)
+    res = {"busbw_gbs": egress / t / 1e9, "ms": t * 1e3, "max_pair_egress_bytes": egress,
+           "workload": f"cfg4 DLRM skewed: local batches {bz} (Zipf 1.1 weights)"}
+    if pg is not None:
+        try:
+            t2 = dev_time(lambda: dist.all_to_all_single(sout, sinp, src, ssc, group=pg))
+            res["nccl_busbw_gbs"] = egress / t2 / 1e9
+        except Exception as exc:  # noqa: BLE001
+            res["nccl_error"] = repr(exc)
+    out["all_to_allv_dlrm_skew"] = res
+
+    # cfg5 mixed-collective step: a2av forward, the 14 DLRM MLP
+    # gradient all_reduces posted async on the fusion backend (B = 1 MiB,
+    # T = 5 ms), all_gatherv i64 (1000 + 137 r), gatherv f32 -> root 0
+    # (16 (r+1)), a2av backward (transposed counts). Device time per step,
+    # max over ranks, host posting included (the step is what a trainer sees).
+    try:
+        mlp = [6656, 512, 262144, 512, 65536, 128, 490496, 1024, 1048576, 1024, 1048576, 1024,
+               1024, 1]
+        grads = [Buffer(torch.randn(k, device=dev)) for k in mlp]
+        agc = [1000 + 137 * q for q in range(world)]
+        agd = [sum(agc[:q]) for q in range(world)]
+        ag_in = Buffer(torch.randint(-1000, 1000, (agc[rank],), dtype=torch.int64, device=dev))
+        ag_out = Buffer(torch.empty(sum(agc), dtype=torch.int64, device=dev))
+        gvc = [16 * (q + 1) for q in range(world)]
+        gvd = [sum(gvc[:q]) for q in range(world)]
+        gv_in = Buffer(torch.randn(gvc[rank], device=dev))
+        gv_out = Buffer(torch.empty(sum(gvc), device=dev))
+        bwd = Buffer(torch.empty(sum(sc), device=dev))
+        log = rt.comm_log
+
+        def step():
+            rt.all_to_allv("nvl", O, I, sc, rc, sd, rdp)
+            hs = [rt.all_reduce("nvl_fused", g, async_op=True) for g in grads]
+            rt.all_gatherv("nvl", ag_out, ag_in, agc, agd)
+            rt.gatherv("nvl", gv_out, gv_in, 0, gvc, gvd)
+            rt.all_to_allv("nvl", bwd, O, rc, sc, rdp, sd)
+            for h in hs:
+                rt.wait(h)
+
+        reps = 20
+        rt.synchronize()
+        n0 = len(log.records())
+        t = dev_time(step, reps=reps)
+        rt.synchronize()
+        recs = log.records()[n0:]
+        fused = [r_ for r_ in recs if r_.backend == "nvl_fused" and r_.fused]
+        steps_logged = reps + 3  # dev_time's warm-up steps included
+        out["mixed_step_cfg5"] = {
+            "step_ms": t * 1e3, "ops_posted_per_step": 18,
+            "fused_flushes_per_step": len(fused) / steps_logged,
+            "fused_members_per_step": sum(r_.members for r_ in fused) / steps_logged,
+            "log_records_per_step": len(recs) / steps_logged,
+            "workload": "cfg5: a2av fwd (cfg4) + 14 MLP-grad all_reduce (fusion B=1MiB, T=5ms) + "
+                        "all_gatherv i64 + gatherv f32 + a2av bwd"}
+    except Exception as exc:  # noqa: BLE001
+        out["mixed_step_cfg5"] = {"error": repr(exc)}
     # DS-MoE cfg3 shape: 4096 tokens x 4096 hidden bf16 per rank, all_to_all_single
     x = torch.randn(4096 * 4096, device=dev).to(torch.bfloat16)
     y = torch.empty_like(x)
