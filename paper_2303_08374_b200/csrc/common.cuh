@@ -68,10 +68,10 @@ struct Pad {
 // epoch and can never be mistaken for a current one (raw bulk payloads could
 // contain any bit pattern, including a small epoch value).
 constexpr size_t kLLOffset = size_t(1) << 20;
-constexpr int64_t kLLMaxPayload = 64 << 10;                // per (sender -> receiver) slot
-constexpr int64_t kLLSlotBytes = 33 * 4096;                // >= 16 + 2 * kLLMaxPayload
+constexpr int64_t kLLMaxPayload = 256 << 10;               // per (sender -> receiver) slot
+constexpr int64_t kLLSlotBytes = 129 * 4096;               // >= 16 + 2 * kLLMaxPayload
 constexpr int64_t kLLParityBytes = int64_t(kMaxRanks) * kLLSlotBytes;
-constexpr size_t kPadBytes = size_t(4) << 20;              // workspace starts 4 MiB in
+constexpr size_t kPadBytes = size_t(16) << 20;             // workspace starts 16 MiB in
 static_assert(sizeof(Pad) <= kLLOffset, "pad too large");
 static_assert(16 + 2 * kLLMaxPayload <= kLLSlotBytes, "LL slot too small");
 static_assert(kLLOffset + 2 * kLLParityBytes <= kPadBytes, "LL area too large");

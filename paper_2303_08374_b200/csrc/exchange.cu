@@ -42,6 +42,7 @@ struct XArgs {
   int gmax;          // communicator-wide cap on CTAs per pair
   int gp;            // CTAs per role in this launch
   int codec;         // 1: trunc16 on peer pairs (2 wire bytes per f32)
+  int64_t ll_max;    // pairs of <= ll_max bytes use LL lines (-1: none)
   uint32_t sig_base;
 };
 
@@ -254,7 +255,7 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
   if (tid == 0 && s_sb[rank] != s_rb[rank]) s_err = MCRDL_ERR_VALIDATION;
   __syncthreads();
   // LL carries small pairs unless the codec is on (LL moves raw bytes)
-  const int64_t ll_max = a.codec ? -1 : kLLMaxPairBytes;
+  const int64_t ll_max = a.ll_max;
   if (s_err) {
     if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
     return;
@@ -264,8 +265,9 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
   const int bid = int(blockIdx.x);
   MCRDL_TRACE_AT(c, bid, 0);
   if (sender) {
-    if (s == 0 && !a.codec)
-      exchange_ll_send_pairs(S.pad, rank, world, par, s_sp, s_sb, a.sig_base, epoch);
+    if (ll_max >= 0)
+      exchange_ll_send_pairs(S.pad, rank, world, par, s_sp, s_sb, a.sig_base, epoch, ll_max, s,
+                             a.gp);
     geo_init(G, s_sw, world, rank, s, a.gmax, slot, ll_max);
     int sent = 0;  // chunks published to peer `me`
     for (int64_t t = 0; t < G.rmax; ++t) {
@@ -314,9 +316,9 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
     block_copy<4>(s_rp[rank] + lo, s_sp[rank] + lo, hi - lo);
   }
   MCRDL_TRACE_AT(c, bid, 1);
-  if (s == 0 && !a.codec) {
+  if (ll_max >= 0) {
     const int e = exchange_ll_recv_pairs(S.pad, rank, world, par, s_rp, s_rb, a.sig_base, epoch,
-                                         c.timeout_ns);
+                                         c.timeout_ns, ll_max, s, a.gp);
     if (e) {  // abort now: other threads may be polling lines that will never come
       atomicCAS(&s_err, 0, e);
       raise_error(S.pad, world, c.err, e, epoch);
@@ -387,7 +389,8 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   }
   mcrdl_status_t st = begin_op(c, stream);
   if (st != MCRDL_OK) return st;
-  if (!sp.codec && try_exchange_ll(c, sp, stream, &st)) return st;
+  const int64_t ll_max = sp.codec ? -1 : exchange_ll_max();
+  if (ll_max >= 0 && try_exchange_ll(c, sp, ll_max, stream, &st)) return st;
   XArgs a;
   memset(&a, 0, sizeof(a));
   for (int r = 0; r < c->world; ++r) {
@@ -403,6 +406,7 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   a.out_count = sp.out_count;
   a.esize = sp.esize;
   a.codec = sp.codec;
+  a.ll_max = ll_max;
   a.sig_base = (sp.sig_base & ~kSigCodecBit) | (sp.codec ? kSigCodecBit : 0u);
   a.slot = c->dc.half_bytes / c->world / 256 * 256;
   a.gmax = c->num_sms < kMaxBlocks ? c->num_sms : kMaxBlocks;  // 2 roles -> 2 CTAs/SM

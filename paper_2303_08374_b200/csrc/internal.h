@@ -164,13 +164,14 @@ mcrdl_status_t launch_exchange(mcrdl_comm* comm, const ExchangeSpec& spec, int64
                                cudaStream_t stream);
 
 // LL protocol (ll.cu) for small messages.
-constexpr int64_t kLLMaxPairBytes = 64 << 10;      // exchange: every pair <= this
+constexpr int64_t kLLMaxPairBytes = 256 << 10;  // measured: tools/ll_ab.sh, profiles/ll_ab_r1_p{2,4}.log      // exchange: every pair <= this
 // Last bytes of each NVLS half: multicast flag words (bcast), zeroed at init.
 constexpr int64_t kNvlsFlagBytes = 64 << 10;
 mcrdl_status_t launch_bcast_nvls(mcrdl_comm* c, uint8_t* buf, int64_t nbytes, int root, int dtype,
                                  uint64_t count, uint64_t seq, cudaStream_t stream);
-constexpr int64_t kLLMaxAllReduceBytes = 64 << 10; // all_reduce one-shot message <= this
-bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, cudaStream_t stream,
+constexpr int64_t kLLMaxAllReduceBytes = 256 << 10; // all_reduce one-shot message <= this
+int64_t exchange_ll_max();
+bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, int64_t ll_max, cudaStream_t stream,
                      mcrdl_status_t* st);
 template <typename T, int OP>
 mcrdl_status_t launch_ar_ll(mcrdl_comm* c, const T* in, T* out, int64_t n,

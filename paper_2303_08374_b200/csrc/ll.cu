@@ -224,14 +224,22 @@ __global__ void __launch_bounds__(kLLThreads) k_exchange_ll(DevComm c, LLArgs a)
 // Returns true when every pair of this rank is an LL pair (the LL kernel
 // then takes the whole op; peers may still run k_exchange for their bulk
 // pairs with other ranks).
-bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, cudaStream_t stream,
+int64_t exchange_ll_max() {
+  // Per-pair LL limit (both ends of a pair decide from its byte count and this
+  // value, identical on every rank). MCRDL_LL_PAIR_BYTES overrides.
+  static const int64_t v = std::min<int64_t>(env_int("MCRDL_LL_PAIR_BYTES", kLLMaxPairBytes),
+                                             kLLMaxPayload);
+  return v;
+}
+
+bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, int64_t ll_max, cudaStream_t stream,
                      mcrdl_status_t* st) {
   int64_t mx = 0;
   for (int r = 0; r < c->world; ++r) {
     if (r == c->rank) continue;
     mx = std::max(mx, std::max(sp.sbytes[r], sp.rbytes[r]));
   }
-  if (sp.d_counts != nullptr || mx > kLLMaxPairBytes) return false;
+  if (sp.d_counts != nullptr || mx > ll_max) return false;
   LLArgs a;
   memset(&a, 0, sizeof(a));
   for (int r = 0; r < c->world; ++r) {
@@ -243,7 +251,7 @@ bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, cudaStream_t stream,
   a.sig_base = sp.sig_base;
   int64_t g = (mx / 8 + kLLThreads * 2 - 1) / (kLLThreads * 2);
   g = std::max<int64_t>(g, (sp.sbytes[c->rank] + (256 << 10) - 1) >> 18);
-  g = std::max<int64_t>(1, std::min<int64_t>(g, 16));
+  g = std::max<int64_t>(1, std::min<int64_t>(g, 64));
   k_exchange_ll<<<int(g), kLLThreads, 0, stream>>>(c->dc, a);
   count_launch();
   cudaError_t e = cudaGetLastError();

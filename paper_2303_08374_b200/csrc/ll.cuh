@@ -138,26 +138,32 @@ __device__ __forceinline__ int ll_recv(const uint8_t* slot, uint8_t* dst, int64_
 
 // Device helpers for the mixed case (k_exchange handles bulk pairs and
 // calls these for its LL pairs from sender / receiver CTA 0).
+// LL pairs (<= ll_max bytes) inside the bulk exchange kernel: CTA b of the
+// role's G CTAs moves units [nu*b/G, nu*(b+1)/G) of every LL pair; CTA 0
+// writes / checks the header.
 __device__ __forceinline__ void exchange_ll_send_pairs(Pad* const* pads, int rank, int world, int par,
                                        const uint8_t* const* sptr, const int64_t* sbytes,
-                                       uint32_t sig_base, uint32_t epoch) {
+                                       uint32_t sig_base, uint32_t epoch, int64_t ll_max, int b,
+                                       int G) {
   for (int k = 1; k < world; ++k) {
     const int j = (rank + k) % world;
     const int64_t B = sbytes[j];
-    if (B > kLLMaxPairBytes) continue;
-    ll_send(ll_slot(pads[j], par, rank), sptr[j], B, 0, (B + 7) / 8, true,
+    if (B > ll_max) continue;
+    const int64_t nu = (B + 7) / 8;
+    ll_send(ll_slot(pads[j], par, rank), sptr[j], B, nu * b / G, nu * (b + 1) / G, b == 0,
             mix32(sig_base, uint64_t(B)), epoch);
   }
 }
 __device__ __forceinline__ int exchange_ll_recv_pairs(Pad* const* pads, int rank, int world, int par,
                                       uint8_t* const* rptr, const int64_t* rbytes, uint32_t sig_base,
-                                      uint32_t epoch, uint64_t tmo) {
+                                      uint32_t epoch, uint64_t tmo, int64_t ll_max, int b, int G) {
   for (int k = 1; k < world; ++k) {
     const int i = (rank - k + world) % world;
     const int64_t B = rbytes[i];
-    if (B > kLLMaxPairBytes) continue;
-    const int e = ll_recv(ll_slot(pads[rank], par, i), rptr[i], B, 0, (B + 7) / 8, true,
-                          mix32(sig_base, uint64_t(B)), epoch, pads[rank], tmo);
+    if (B > ll_max) continue;
+    const int64_t nu = (B + 7) / 8;
+    const int e = ll_recv(ll_slot(pads[rank], par, i), rptr[i], B, nu * b / G, nu * (b + 1) / G,
+                          b == 0, mix32(sig_base, uint64_t(B)), epoch, pads[rank], tmo);
     if (e) return e;
   }
   return 0;
