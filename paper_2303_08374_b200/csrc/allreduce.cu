@@ -1371,7 +1371,14 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
       // (MCRDL_AR_GPMAX / MCRDL_AR_CHUNK_KB override, for tuning).
       int64_t gp = (sp * 16 + (32 << 10) - 1) / (32 << 10);
       static const int64_t gp_env = env_int("MCRDL_AR_GPMAX", 0);
-      static const int64_t chunk_kb = env_int("MCRDL_AR_CHUNK_KB", 256);
+      // Flag chunk: 256 KiB, but 128 KiB for mid-size launches at p >= 4 so a
+      // CTA share spans several rows and RS / AG overlap (tools/chunk_ab.sh,
+      // profiles/chunk_ab_r1_p{2,4}.log: p = 4, 64 MiB 464 vs 439 GB/s; 256 MiB
+      // and p = 2 prefer 256 KiB). MCRDL_AR_CHUNK_KB overrides.
+      static const int64_t chunk_env = env_int("MCRDL_AR_CHUNK_KB", 0);
+      const int64_t chunk_kb =
+          chunk_env > 0 ? chunk_env
+                        : (world >= 4 && m * int64_t(sizeof(T)) < (int64_t(128) << 20) ? 128 : 256);
       int64_t gmax = gp_env > 0 ? gp_env : 2 * c->num_sms / 3;
       if (gmax > kMaxBlocks) gmax = kMaxBlocks;
       if (gmax < 1) gmax = 1;
