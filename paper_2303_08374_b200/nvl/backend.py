@@ -17,6 +17,7 @@ native library or a CUDA device is missing, init raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 import time
 from ctypes import byref, c_void_p
@@ -387,7 +388,9 @@ class NvlBackendInstance:
 
     # ------------------------------------------- pipelined host staging
     PIPE_MIN_BYTES = 16 << 20
-    PIPE_CHUNK_BYTES = 32 << 20
+    # H2D -> collective -> D2H chunk: pipeline fill + drain cost one chunk of
+    # PCIe each way (MCRDL_PIPE_CHUNK_MB overrides)
+    PIPE_CHUNK_BYTES = int(os.environ.get("MCRDL_PIPE_CHUNK_MB", "32")) << 20
 
     def _pipelined_ok(self, req: CommRequest) -> bool:
         """Large all_reduce on pinned host tensors: overlap H2D, the collective
@@ -402,7 +405,7 @@ class NvlBackendInstance:
     def _post_pipelined(self, req: CommRequest, handle: WorkHandle) -> None:
         dt = req.input.dtype
         n = req.input.count
-        k = max(2, min(32, req.input.nbytes // self.PIPE_CHUNK_BYTES))
+        k = max(2, min(64, req.input.nbytes // self.PIPE_CHUNK_BYTES))
         step = ((n + k - 1) // k + 63) // 64 * 64
         h_in, h_out = req.input.array, req.output.array
         lane = self.stream

@@ -164,6 +164,23 @@ int main(int argc, char** argv) {
       printf("%-6s %2d %5d %9.4f %10.1f %10.1f %12.1f\n", v.name, v.u, g, best, alg, bus, link);
     }
   }
+  // single-source multicast store: only GPU 0 stores the WHOLE buffer (the
+  // NVLS bcast root's egress); others idle
+  for (int g : grids) {
+    float best = 1e30f;
+    for (int it = 0; it < 4; ++it) {
+      for (int d = 0; d < N; ++d) { CK(cudaSetDevice(d)); CK(cudaDeviceSynchronize()); }
+      CK(cudaSetDevice(0));
+      CK(cudaEventRecord(e0[0], st[0]));
+      k_nvls<4><<<g, 512, 0, st[0]>>>(2, mcva[0], scratch[0], int64_t(bytes) / 16);
+      CK(cudaEventRecord(e1[0], st[0]));
+      CK(cudaEventSynchronize(e1[0]));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0[0], e1[0]));
+      if (it > 0) best = std::min(best, ms);
+    }
+    printf("st1    %2d %5d %9.4f  root egress %8.1f GB/s\n", 4, g, best, double(bytes) / (best * 1e-3) / 1e9);
+  }
   // sanity: after rsag, every element = sum(d+1) * (#rsag iterations) ... just check finite
   CK(cudaSetDevice(0));
   float h = 0;
