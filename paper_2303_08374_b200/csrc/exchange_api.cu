@@ -2,6 +2,8 @@
 // reference collective onto per-peer (pointer, bytes) spans.
 #include <string.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace mcrdl {
@@ -23,6 +25,13 @@ static int split_codec(mcrdl_algo_t* algo, mcrdl_dtype_t dtype) {
   const int f = int(*algo);
   *algo = mcrdl_algo_t(f & 0xFF);
   return ((f & MCRDL_CODEC_TRUNC16) != 0 && dtype == MCRDL_F32) ? 1 : 0;
+}
+
+// Pair sizes where storing straight into symmetric outputs beats the staged
+// exchange (measured, profiles/symmx_perf_r1.log: +5-13 % for 4-128 MiB
+// pairs; below, LL / staged latency wins; above, -2-3 %). Agreed by all ranks.
+static bool symm_x_window(int64_t pair_bytes) {
+  return pair_bytes > (int64_t(4) << 20) && pair_bytes <= (int64_t(128) << 20);
 }
 
 static ExchangeSpec empty_spec(int esize, uint32_t sig_base) {
@@ -101,6 +110,19 @@ mcrdl_status_t mcrdl_all_to_all_single(mcrdl_comm* c, const void* in, void* out,
   if (in == out && c->world > 1 && count > 0)
     return set_error(MCRDL_ERR_VALIDATION, "in-place all_to_all_single: pass a snapshot of the input");
   const int64_t m = int64_t(count) / c->world;
+  if (!codec && symm_x_window(m * es)) {  // symmetric output: zero-copy direct write
+    int64_t so[kMaxRanks], ro[kMaxRanks], b[kMaxRanks];
+    for (int q = 0; q < c->world; ++q) {
+      so[q] = int64_t(q) * m * es;
+      ro[q] = int64_t(c->rank) * m * es;
+      b[q] = m * es;
+    }
+    mcrdl_status_t st;
+    if (try_exchange_symm(c, in, out, uint64_t(count) * es, so, ro, b, m * es,
+                          op_sig(kKindA2ASingle, dtype, 1, -1, uint64_t(m), seq),
+                          reinterpret_cast<cudaStream_t>(stream), &st))
+      return st;
+  }
   ExchangeSpec s = empty_spec(es, op_sig(kKindA2ASingle, dtype, 0, -1, uint64_t(m), seq));
   s.codec = codec;
   for (int r = 0; r < c->world; ++r) {
@@ -144,6 +166,26 @@ mcrdl_status_t mcrdl_all_gatherv(mcrdl_comm* c, const void* in, void* out, const
   const int es = elem_size(dtype);
   if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
   if (!check_counts(rcounts, displs, c->world, "rcounts")) return MCRDL_ERR_VALIDATION;
+  {  // symmetric output: every rank stores its block straight into every output
+    int64_t mx = 0, end = 0;
+    for (int r = 0; r < c->world; ++r) {
+      mx = std::max<int64_t>(mx, rcounts[r] * es);
+      end = std::max<int64_t>(end, (displs[r] + rcounts[r]) * es);
+    }
+    if (!codec && symm_x_window(mx)) {
+      int64_t so[kMaxRanks], ro[kMaxRanks], b[kMaxRanks];
+      for (int q = 0; q < c->world; ++q) {
+        so[q] = 0;
+        ro[q] = displs[c->rank] * es;
+        b[q] = rcounts[c->rank] * es;
+      }
+      mcrdl_status_t st;
+      if (try_exchange_symm(c, in, out, uint64_t(end), so, ro, b, mx,
+                            op_sig(kKindAllGatherv, dtype, 1, -1, 0, seq),
+                            reinterpret_cast<cudaStream_t>(stream), &st))
+        return st;
+    }
+  }
   ExchangeSpec s = empty_spec(es, op_sig(kKindAllGatherv, dtype, 0, -1, 0, seq));
   s.codec = codec;
   int64_t total = 0;

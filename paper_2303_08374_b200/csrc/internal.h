@@ -171,6 +171,9 @@ mcrdl_status_t launch_bcast_nvls(mcrdl_comm* c, uint8_t* buf, int64_t nbytes, in
                                  uint64_t count, uint64_t seq, cudaStream_t stream);
 constexpr int64_t kLLMaxAllReduceBytes = 256 << 10; // all_reduce one-shot message <= this
 int64_t exchange_ll_max();
+bool try_exchange_symm(mcrdl_comm* c, const void* in, void* out, uint64_t out_bytes,
+                       const int64_t* send_off, const int64_t* recv_off, const int64_t* bytes,
+                       int64_t grid_bytes, uint32_t sig, cudaStream_t stream, mcrdl_status_t* st);
 bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, int64_t ll_max, cudaStream_t stream,
                      mcrdl_status_t* st);
 template <typename T, int OP>

@@ -133,9 +133,21 @@ def make_op(rt, backend: str, kind: CommOpKind, nbytes: int, dtype: DType,
     if kind is CommOpKind.bcast:
         b = Buffer(t(n))
         return lambda: rt.bcast(backend, b, 0)
+    def out_t(count):  # symmetric output (zero-copy exchange) when asked
+        if not symmetric:
+            return t(count)
+        key = (backend, "out", count, dtype)
+        if key not in _SYMM_CACHE:
+            _SYMM_CACHE[key] = rt.symmetric_empty(backend, count, dtype)
+        return _SYMM_CACHE[key]
+
+    if kind is CommOpKind.all_to_all_single:
+        m = max(n // p, 1)
+        i, o = Buffer(t(m * p)), Buffer(out_t(m * p))
+        return lambda: rt.all_to_all_single(backend, o, i)
     if kind in (CommOpKind.all_gatherv, CommOpKind.all_gather):
         m = max(n // p, 1)
-        i, o = Buffer(t(m)), Buffer(t(m * p))
+        i, o = Buffer(t(m)), Buffer(out_t(m * p))
         counts, displs = [m] * p, [k * m for k in range(p)]
         return lambda: rt.all_gatherv(backend, o, i, counts, displs)
     if kind in (CommOpKind.all_to_allv, CommOpKind.all_to_all_single):

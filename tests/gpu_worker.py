@@ -675,6 +675,31 @@ def sc_symm(cx: Ctx):
                     else:
                         cx.check(tag, from_dev(dst, dtype), want)
     inst.policy = AlgorithmPolicy()
+    # exchanges into symmetric outputs (csrc/symm_x.cu: senders store straight
+    # into every peer's output above the LL pair size; LL below)
+    for dtype, m, off in ((DType.f32, (5 << 20) // 4 + 3, 0), (DType.i64, (5 << 20) // 8 + 1, 1),
+                          (DType.bf16, 3 << 20, 0), (DType.f32, 100_003, 0), (DType.f32, 1000, 0)):
+        ins = [values(dtype, p * m, "symm-a2a", dtype.name, m, q) for q in range(p)]
+        src = to_dev(ins[r], dtype, dev)
+        dst = view(B, dtype, p * m, off)
+        dst.zero_()
+        cx.rt.all_to_all_single(cx.b, Buffer(dst), Buffer(src))
+        cx.check(f"symm/a2a_single/{dtype.name}/{m}/off{off}", from_dev(dst, dtype),
+                 seqref.all_to_all_single(ins)[r])
+    # in place on a symmetric buffer (the input is snapshotted, the output is symmetric)
+    m = (5 << 20) // 4 + 7
+    ins = [values(DType.f32, p * m, "symm-a2a-ip", q) for q in range(p)]
+    io = view(A, DType.f32, p * m)
+    io.copy_(to_dev(ins[r], DType.f32, dev))
+    bb = Buffer(io)
+    cx.rt.post(CommRequest(CommOpKind.all_to_all_single, input=bb, output=bb, backend=cx.b))
+    cx.check("symm/a2a_single/inplace", from_dev(io, DType.f32), seqref.all_to_all_single(ins)[r])
+    counts = [(5 << 20) // 4 + 1013 * q for q in range(p)]
+    displs = packed(counts)
+    ins = [values(DType.f32, counts[q], "symm-agv", q) for q in range(p)]
+    dst = view(B, DType.f32, sum(counts), 3)
+    cx.rt.all_gatherv(cx.b, Buffer(dst), Buffer(to_dev(ins[r], DType.f32, dev)), counts, displs)
+    cx.check("symm/all_gatherv", from_dev(dst, DType.f32), seqref.all_gatherv(ins, counts, displs)[r])
     # symmetric input, ordinary output: the standard (staged) path
     n = 100_003
     ins = [values(DType.i64, n, "symm-mixed", q) for q in range(p)]
