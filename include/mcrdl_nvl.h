@@ -222,8 +222,9 @@ mcrdl_status_t mcrdl_barrier(mcrdl_comm* comm, uint64_t seq, void* stream);
 /* Point-to-point (Runtime.send / Runtime.recv, runtime.py:498-508, executed by
  * BackendInstance.execute, runtime.py:244-262). Only the two endpoints take
  * part; no collective sequence number is consumed. Messages are matched in
- * post order per (sender, receiver) pair. send is eager up to 256 queued
- * messages and the per-sender mailbox (MCRDL_P2P_BYTES, default 32 MiB) and
+ * post order per (sender, receiver) pair. send is eager: messages <= 256 KiB
+ * (LL path) up to 64 outstanding, larger ones up to 256 queued messages and
+ * the per-sender mailbox (MCRDL_P2P_BYTES, default 32 MiB); beyond that it
  * streams larger messages through it (the matching recv must then be in
  * flight: post it first, on another stream). Sends, receives and collectives
  * are ordered only within their own kind, so a recv may overlap a send. A byte-count

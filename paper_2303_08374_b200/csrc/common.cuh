@@ -35,8 +35,8 @@ constexpr int64_t kP2PChunk = 64 << 10;  // one CTA pass (512 thr x 16 B x 8)
 constexpr int kP2PHdr = 256;
 // Small messages (<= kP2PLLMax bytes) take the LL path: a ring of kP2PLLSlots
 // slots per sender, each a header line + 16-byte {data, tag} lines.
-constexpr int kP2PLLSlots = 128;
-constexpr int64_t kP2PLLMax = 64 << 10;
+constexpr int kP2PLLSlots = 64;
+constexpr int64_t kP2PLLMax = 256 << 10;
 constexpr int64_t kP2PLLCtaBytes = 8 << 10;  // payload per CTA of an LL message
 constexpr int64_t kP2PLLSlotBytes = 2 * kP2PLLMax + 256;
 constexpr int64_t kP2PLLSenderBytes = int64_t(kP2PLLSlots) * kP2PLLSlotBytes;
