@@ -756,15 +756,24 @@ __device__ __forceinline__ void ar_nvls_body(DevComm c, uint8_t* uc, uint8_t* mc
       }
       const int64_t lo = int64_t(r) * chp, hi = min(len, lo + chp);
       const int64_t base = int64_t(rank) * sp + rb;
+      // own segment: the result goes to the peers through the switch and
+      // straight into `out` here (the gatherers skip it)
       int64_t i = lo + tid;
       for (; i + 3 * nt < hi; i += 4 * nt) {
         uint4 v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) v[u] = mm_ld_reduce_sum<T>(mc + (base + i + u * nt) * 16);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) mm_st(mc + (base + i + u * nt) * 16, v[u]);
+        for (int u = 0; u < 4; ++u) {
+          mm_st(mc + (base + i + u * nt) * 16, v[u]);
+          store_pack<T, VEC>(out, base + i + u * nt, n, v[u]);
+        }
       }
-      for (; i < hi; i += nt) mm_st(mc + (base + i) * 16, mm_ld_reduce_sum<T>(mc + (base + i) * 16));
+      for (; i < hi; i += nt) {
+        const uint4 v = mm_ld_reduce_sum<T>(mc + (base + i) * 16);
+        mm_st(mc + (base + i) * 16, v);
+        store_pack<T, VEC>(out, base + i, n, v);
+      }
       if (fence) __threadfence_system();  // multicast stores complete on every rank before the flag
       __syncthreads();
       if (tid < world) publish(&S.pad[tid]->flag2[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
@@ -792,6 +801,7 @@ __device__ __forceinline__ void ar_nvls_body(DevComm c, uint8_t* uc, uint8_t* mc
         return;
       }
       for (int q = 0; q < world; ++q) {
+        if (q == rank) continue;  // written by this rank's reducer
         const int64_t len = seg_len(npk, sp, q, rb, re);
         const int64_t lo = int64_t(r) * chp;
         if (lo >= len) continue;
