@@ -43,6 +43,8 @@ struct XArgs {
   int gp;            // CTAs per role in this launch
   int codec;         // 1: trunc16 on peer pairs (2 wire bytes per f32)
   int64_t ll_max;    // pairs of <= ll_max bytes use LL lines (-1: none)
+  int64_t pair_cta;  // bytes of a pair per serving CTA (kPairCtaBytes)
+  int64_t chunk_min; // minimum flag chunk (kChunkBytes)
   uint32_t sig_base;
 };
 
@@ -115,18 +117,18 @@ __device__ __forceinline__ void block_decode16(uint8_t* dst, const uint8_t* src,
   for (int64_t e = done + tid; e < ne; e += nt) d32[e] = uint32_t(__ldcg(s16 + e)) << 16;
 }
 // CTAs serving one pair: a function of the pair's byte count only.
-__device__ __host__ __forceinline__ int pair_ctas(int64_t bytes, int gmax) {
-  int64_t g = (bytes + kPairCtaBytes - 1) / kPairCtaBytes;
+__device__ __host__ __forceinline__ int pair_ctas(int64_t bytes, int gmax, int64_t per_cta) {
+  int64_t g = (bytes + per_cta - 1) / per_cta;
   return int(g < 1 ? 1 : (g > gmax ? gmax : g));
 }
-__device__ __forceinline__ int64_t pair_chunk(int64_t bytes, int g) {
+__device__ __forceinline__ int64_t pair_chunk(int64_t bytes, int g, int64_t chunk_min) {
   // (~4 smaller chunks per share for push / copy-out overlap measured WORSE
   // for mid-size pairs: p = 4 all_to_allv 16 MiB 275 vs 325 GB/s — the extra
   // flag round trips cost more than the overlap gains)
   int64_t per = (bytes + g - 1) / g;
   int64_t ch = (per + kMaxSteps - 1) / kMaxSteps;
   ch = (ch + 15) & ~int64_t(15);
-  return ch > kChunkBytes ? ch : kChunkBytes;
+  return ch > chunk_min ? ch : chunk_min;
 }
 
 // Share s of round t of a pair moving B bytes: [a, e) relative to the round,
@@ -170,13 +172,14 @@ struct PeerGeo {
 };
 
 __device__ __forceinline__ void geo_init(PeerGeo& G, const int64_t* bytes, int world, int rank,
-                                         int s, int gmax, int64_t slot, int64_t ll_max) {
+                                         int s, int gmax, int64_t slot, int64_t ll_max,
+                                         int64_t per_cta, int64_t chunk_min) {
   const int tid = threadIdx.x;
   if (tid < world) {
     const int64_t B = bytes[tid];
-    const int g = pair_ctas(B, gmax);
+    const int g = pair_ctas(B, gmax, per_cta);
     G.g[tid] = g;
-    G.ch[tid] = pair_chunk(B, g);
+    G.ch[tid] = pair_chunk(B, g, chunk_min);
     // LL pairs (<= kLLMaxPairBytes, ll.cuh) are moved by CTA 0 of each role.
     G.R[tid] = (tid != rank && s < g && B > ll_max) ? rounds_for(B, slot) : 0;
   }
@@ -268,7 +271,7 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
     if (ll_max >= 0)
       exchange_ll_send_pairs(S.pad, rank, world, par, s_sp, s_sb, a.sig_base, epoch, ll_max, s,
                              a.gp);
-    geo_init(G, s_sw, world, rank, s, a.gmax, slot, ll_max);
+    geo_init(G, s_sw, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min);
     int sent = 0;  // chunks published to peer `me`
     for (int64_t t = 0; t < G.rmax; ++t) {
       if (t > 0) {  // slot reuse: receiver share s consumed round t-1
@@ -329,7 +332,7 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
     if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
     return;
   }
-  geo_init(G, s_rw, world, rank, s, a.gmax, slot, ll_max);
+  geo_init(G, s_rw, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min);
   int got = 0;  // chunks consumed from peer `me`
   const uint8_t* my_ws = S.ws[rank] + hoff;
   for (int64_t t = 0; t < G.rmax; ++t) {
@@ -407,6 +410,11 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   a.esize = sp.esize;
   a.codec = sp.codec;
   a.ll_max = ll_max;
+  // Geometry knobs (tools/xgeo_ab.sh); every rank must see the same values.
+  static const int64_t pair_kb = env_int("MCRDL_X_PAIR_KB", kPairCtaBytes >> 10);
+  static const int64_t chunk_kb = env_int("MCRDL_X_CHUNK_KB", kChunkBytes >> 10);
+  a.pair_cta = (pair_kb > 0 ? pair_kb : kPairCtaBytes >> 10) << 10;
+  a.chunk_min = (chunk_kb > 0 ? chunk_kb : kChunkBytes >> 10) << 10;
   a.sig_base = (sp.sig_base & ~kSigCodecBit) | (sp.codec ? kSigCodecBit : 0u);
   a.slot = c->dc.half_bytes / c->world / 256 * 256;
   a.gmax = c->num_sms < kMaxBlocks ? c->num_sms : kMaxBlocks;  // 2 roles -> 2 CTAs/SM
@@ -423,8 +431,8 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
         g = std::max<int64_t>(g, std::min<int64_t>(a.gmax, (sp.sbytes[r] + (1 << 20) - 1) >> 20));
         continue;
       }
-      g = std::max<int64_t>(g, pair_ctas(sp.sbytes[r], a.gmax));
-      g = std::max<int64_t>(g, pair_ctas(sp.rbytes[r], a.gmax));
+      g = std::max<int64_t>(g, pair_ctas(sp.sbytes[r], a.gmax, a.pair_cta));
+      g = std::max<int64_t>(g, pair_ctas(sp.rbytes[r], a.gmax, a.pair_cta));
     }
   }
   a.gp = int(g);
