@@ -49,7 +49,10 @@ struct XArgs {
 };
 
 constexpr int64_t kPairCtaBytes = 32 << 10;   // one CTA per 32 KiB of a pair
-constexpr int64_t kChunkBytes = 256 << 10;    // flag granularity inside a share
+// Flag granularity inside a share: 128 KiB (p = 4 all_to_allv 256 MiB: 393 vs
+// 418 us at 256 KiB, 64 KiB equal to 128 KiB, <= 16 MiB neutral;
+// profiles/xgeo_ab_r1_p4.log).
+constexpr int64_t kChunkBytes = 128 << 10;
 constexpr int64_t kMaxSteps = 4000;           // < 4096 (12-bit flag step)
 
 __device__ __host__ __forceinline__ int64_t rounds_for(int64_t bytes, int64_t slot) {
