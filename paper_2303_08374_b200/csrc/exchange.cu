@@ -45,6 +45,7 @@ struct XArgs {
   int64_t ll_max;    // pairs of <= ll_max bytes use LL lines (-1: none)
   int64_t pair_cta;  // bytes of a pair per serving CTA (kPairCtaBytes)
   int64_t chunk_min; // minimum flag chunk (kChunkBytes)
+  int64_t wide_min;  // pairs of >= wide_min bytes get 4x pair_cta per CTA (0: off)
   uint32_t sig_base;
 };
 
@@ -120,7 +121,9 @@ __device__ __forceinline__ void block_decode16(uint8_t* dst, const uint8_t* src,
   for (int64_t e = done + tid; e < ne; e += nt) d32[e] = uint32_t(__ldcg(s16 + e)) << 16;
 }
 // CTAs serving one pair: a function of the pair's byte count only.
-__device__ __host__ __forceinline__ int pair_ctas(int64_t bytes, int gmax, int64_t per_cta) {
+__device__ __host__ __forceinline__ int pair_ctas(int64_t bytes, int gmax, int64_t per_cta,
+                                                  int64_t wide_min) {
+  if (wide_min > 0 && bytes >= wide_min) per_cta *= 4;
   int64_t g = (bytes + per_cta - 1) / per_cta;
   return int(g < 1 ? 1 : (g > gmax ? gmax : g));
 }
@@ -176,11 +179,11 @@ struct PeerGeo {
 
 __device__ __forceinline__ void geo_init(PeerGeo& G, const int64_t* bytes, int world, int rank,
                                          int s, int gmax, int64_t slot, int64_t ll_max,
-                                         int64_t per_cta, int64_t chunk_min) {
+                                         int64_t per_cta, int64_t chunk_min, int64_t wide_min) {
   const int tid = threadIdx.x;
   if (tid < world) {
     const int64_t B = bytes[tid];
-    const int g = pair_ctas(B, gmax, per_cta);
+    const int g = pair_ctas(B, gmax, per_cta, wide_min);
     G.g[tid] = g;
     G.ch[tid] = pair_chunk(B, g, chunk_min);
     // LL pairs (<= kLLMaxPairBytes, ll.cuh) are moved by CTA 0 of each role.
@@ -274,7 +277,7 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
     if (ll_max >= 0)
       exchange_ll_send_pairs(S.pad, rank, world, par, s_sp, s_sb, a.sig_base, epoch, ll_max, s,
                              a.gp);
-    geo_init(G, s_sw, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min);
+    geo_init(G, s_sw, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min, a.wide_min);
     int sent = 0;  // chunks published to peer `me`
     for (int64_t t = 0; t < G.rmax; ++t) {
       if (t > 0) {  // slot reuse: receiver share s consumed round t-1
@@ -335,7 +338,7 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
     if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
     return;
   }
-  geo_init(G, s_rw, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min);
+  geo_init(G, s_rw, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min, a.wide_min);
   int got = 0;  // chunks consumed from peer `me`
   const uint8_t* my_ws = S.ws[rank] + hoff;
   for (int64_t t = 0; t < G.rmax; ++t) {
@@ -418,6 +421,11 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   static const int64_t chunk_kb = env_int("MCRDL_X_CHUNK_KB", kChunkBytes >> 10);
   a.pair_cta = (pair_kb > 0 ? pair_kb : kPairCtaBytes >> 10) << 10;
   a.chunk_min = (chunk_kb > 0 ? chunk_kb : kChunkBytes >> 10) << 10;
+  // Pairs >= 8 MiB: 128 KiB of pair per CTA (fewer, longer shares). p = 4
+  // 32/64 MiB all_to_allv +11/+8 %, p = 2 16/32 MiB +17/+13 %, other sizes
+  // neutral; a 4 MiB threshold costs p = 4 16 MiB (profiles/xwide_ab_r1_p2p4.log).
+  static const int64_t wide_mb = env_int("MCRDL_X_WIDE_MB", 8);
+  a.wide_min = wide_mb > 0 ? wide_mb << 20 : 0;
   a.sig_base = (sp.sig_base & ~kSigCodecBit) | (sp.codec ? kSigCodecBit : 0u);
   a.slot = c->dc.half_bytes / c->world / 256 * 256;
   a.gmax = c->num_sms < kMaxBlocks ? c->num_sms : kMaxBlocks;  // 2 roles -> 2 CTAs/SM
@@ -434,8 +442,12 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
         g = std::max<int64_t>(g, std::min<int64_t>(a.gmax, (sp.sbytes[r] + (1 << 20) - 1) >> 20));
         continue;
       }
-      g = std::max<int64_t>(g, pair_ctas(sp.sbytes[r], a.gmax, a.pair_cta));
-      g = std::max<int64_t>(g, pair_ctas(sp.rbytes[r], a.gmax, a.pair_cta));
+      // wire bytes, as the kernel computes them: pair_ctas is not monotonic
+      // in the byte count (wide pairs), so user bytes would under-size the grid
+      const int64_t sw = sp.codec ? sp.sbytes[r] / 2 : sp.sbytes[r];
+      const int64_t rw = sp.codec ? sp.rbytes[r] / 2 : sp.rbytes[r];
+      g = std::max<int64_t>(g, pair_ctas(sw, a.gmax, a.pair_cta, a.wide_min));
+      g = std::max<int64_t>(g, pair_ctas(rw, a.gmax, a.pair_cta, a.wide_min));
     }
   }
   a.gp = int(g);
