@@ -5,4 +5,4 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')
 timeout 600 python bench.py > gpurun_out/r1z_bench_n1.log 2>&1
 timeout 600 python bench.py --impl reference > gpurun_out/r1z_ref_n1.log 2>&1
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29555 bench.py --gpus 4 --steps 10 --warmup 3 > gpurun_out/r1z_bench_n4.log 2>&1
-tail -3 gpurun_out/r1z_*.log
+tail -n 3 gpurun_out/r1z_*.log
