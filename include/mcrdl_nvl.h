@@ -103,9 +103,10 @@ typedef struct {
   int rank;
   int world;
   int device;
-  int num_sms;
+  int num_sms;               /* SM budget launches are sized from (device SMs,
+                                split between co-located ranks, MCRDL_MAX_SMS) */
   int nvls_supported;        /* NVSwitch multicast object usable */
-  int reserved0;
+  int ranks_per_device;      /* >1: ranks share a GPU (co-located test mode) */
   uint64_t workspace_bytes;  /* symmetric workspace per rank (two halves) */
   uint64_t max_oneshot_bytes;/* largest all_reduce the one-shot path takes */
   uint64_t max_twoshot_chunk;/* per-launch all_reduce chunk for two-shot   */
@@ -122,6 +123,12 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** comm, int rank, int world, int cuda_
 /* Reference: BackendInstance.finalize (runtime.py:279-290). */
 mcrdl_status_t mcrdl_comm_destroy(mcrdl_comm* comm);
 mcrdl_status_t mcrdl_comm_caps(const mcrdl_comm* comm, mcrdl_caps_t* caps);
+/* The communicator's own non-blocking CUDA streams (created at init,
+ * destroyed with the comm): which = 0 the host layer's progress lane for async
+ * posts (reference: the per-backend lane thread, runtime.py:117-126), 1 / 2 the
+ * H2D / D2H staging streams of pipelined host-buffer posts. Never shared
+ * between communicators. */
+mcrdl_status_t mcrdl_comm_stream(const mcrdl_comm* comm, int which, void** stream);
 /* Latched device error (order mismatch / timeout) of every op issued so far,
  * read without a device sync: call after the stream work completed
  * (WorkHandle.wait / Runtime.synchronize, core.py:312-319, runtime.py:470-494).

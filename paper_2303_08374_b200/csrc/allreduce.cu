@@ -248,7 +248,7 @@ __device__ __forceinline__ void tma_drain() {
 
 template <typename T, int OP, bool VEC, bool TMA>
 __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int64_t n, int64_t sp,
-                                             int64_t segb, int gp, int gs, int64_t chp, int ag_pull,
+                                             int64_t segb, int gp, int gs, int64_t chp,
                                              int root, uint32_t epoch, uint32_t sig, T* rs_out,
                                              int64_t rs_n) {
   constexpr int N = Pack<T>::N;
@@ -395,13 +395,9 @@ __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int
               st16(S.ws[root] + hoff + ag + int64_t(rank) * segb + i * 16, res);
             continue;
           }
-          if (ag_pull) {  // peers pull it from my workspace
-            st16(S.ws[rank] + hoff + ag + int64_t(rank) * segb + i * 16, res);
-          } else {
-            for (int k = 1; k < world; ++k) {
-              const int q = (rank + k) % world;
-              st16(S.ws[q] + hoff + ag + int64_t(rank) * segb + i * 16, res);
-            }
+          for (int k = 1; k < world; ++k) {
+            const int q = (rank + k) % world;
+            st16(S.ws[q] + hoff + ag + int64_t(rank) * segb + i * 16, res);
           }
           store_pack<T, VEC>(out, int64_t(rank) * sp + i, n, res);
         }
@@ -441,18 +437,6 @@ __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int
       if (lo >= len) continue;
       const int64_t hi = min(len, lo + chp);
       int64_t i = rb + lo + tid;
-      if (ag_pull) {  // remote reads of rank q's reduced segment: 8 packs in flight
-        const uint8_t* src = S.ws[q] + hoff + ag + int64_t(q) * segb;
-        for (; i + 7 * nt < rb + hi; i += 8 * nt) {
-          uint4 v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = ld16_cg(src + (i + u * nt) * 16);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) store_pack<T, VEC>(out, int64_t(q) * sp + i + u * nt, n, v[u]);
-        }
-        for (; i < rb + hi; i += nt) store_pack<T, VEC>(out, int64_t(q) * sp + i, n, ld16_cg(src + i * 16));
-        continue;
-      }
       const uint8_t* src = ws + ag + int64_t(q) * segb;
       for (; i + 3 * nt < rb + hi; i += 4 * nt) {
         uint4 v[4];
@@ -471,187 +455,11 @@ __device__ __forceinline__ void ar_pipe_body(DevComm c, const T* in, T* out, int
 template <typename T, int OP, bool VEC, bool TMA>
 __global__ void __launch_bounds__(kThreads, 2)
     k_ar_pipe(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int gp, int gs,
-              int64_t chp, int ag_pull, int root, uint32_t sig, T* rs_out = nullptr,
+              int64_t chp, int root, uint32_t sig, T* rs_out = nullptr,
               int64_t rs_n = 0) {
   const uint32_t epoch = epoch_enter(c);
-  ar_pipe_body<T, OP, VEC, TMA>(c, in, out, n, sp, segb, gp, gs, chp, ag_pull, root, epoch, sig,
+  ar_pipe_body<T, OP, VEC, TMA>(c, in, out, n, sp, segb, gp, gs, chp, root, epoch, sig,
                                 rs_out, rs_n);
-  epoch_exit(c, epoch);
-}
-
-// ------------------------------------- warp-specialized two-shot (K2, v3)
-// Same three roles as k_ar_pipe, but inside EVERY CTA as warp groups
-// (senders | reducers | gatherers) synchronised with named barriers, one
-// share per CTA. Measured with tools/trace_ar.py: when roles are whole CTAs,
-// the SMs they share are loaded unevenly and the slowest static share sets
-// the op time (p=2: sender row time p10 56 us vs p90 100 us). Here every SM
-// carries the same mix and the groups never wait for each other locally, only
-// for their peers' flags.
-template <int WS, int WR>
-struct WsRoles {
-  static constexpr int kSend = WS * 32, kRed = WR * 32, kGath = kThreads - (WS + WR) * 32;
-};
-
-template <typename T, bool VEC>
-__device__ __forceinline__ void push_packs_g(const T* in, int64_t n, int64_t g0, int64_t cnt,
-                                             uint8_t* dst, int gtid, int gnt) {
-  int64_t i = gtid;
-  for (; i + 3 * gnt < cnt; i += 4 * gnt) {
-    uint4 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = load_pack<T, VEC>(in, g0 + i + u * gnt, n);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) st16(dst + (i + u * gnt) * 16, v[u]);
-  }
-  for (; i < cnt; i += gnt) st16(dst + i * 16, load_pack<T, VEC>(in, g0 + i, n));
-}
-
-template <typename T, int OP, bool VEC>
-__device__ __forceinline__ void ar_ws_body(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int64_t chp,
-            uint32_t epoch, uint32_t sig) {
-  constexpr int N = Pack<T>::N;
-  constexpr int WS = 6, WR = 6;
-  using Roles = WsRoles<WS, WR>;
-  __shared__ int s_gerr[3];  // per group: written by the group's waiters before its barrier
-  __shared__ SComm S;
-  const int par = epoch & 1, rank = c.rank, world = c.world;
-  const int warp = int(threadIdx.x) >> 5;
-  const int role = warp < WS ? 0 : (warp < WS + WR ? 1 : 2);
-  const int gbase = role == 0 ? 0 : (role == 1 ? Roles::kSend : Roles::kSend + Roles::kRed);
-  const int gnt = role == 0 ? Roles::kSend : (role == 1 ? Roles::kRed : Roles::kGath);
-  const int gtid = int(threadIdx.x) - gbase;
-  const int bar_id = 1 + role;
-  const int s = blockIdx.x, gp = gridDim.x;
-  const int64_t npk = (n + N - 1) / N;
-  const int64_t rb = sp * s / gp, re = sp * (s + 1) / gp;
-  const int64_t hoff = int64_t(par) * c.half_bytes;
-  const int64_t ag = int64_t(world) * segb;
-  if (threadIdx.x < 3) s_gerr[threadIdx.x] = 0;
-  stage_comm(c, S);
-  __syncthreads();  // the last barrier shared by all roles
-  const uint8_t* ws = S.ws[rank] + hoff;
-  MCRDL_TRACE_AT(c, s, 0);
-  auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(gnt) : "memory"); };
-  volatile int* verr = &s_gerr[role];
-  int* s_err_p = &s_gerr[role];
-
-  if (role == 0) {  // ------------------------------------------ senders
-    int rows = 0;
-    for (int q = 0; q < world; ++q)
-      if (q != rank) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
-    for (int r = 0; r < rows; ++r) {
-      for (int k = 1; k < world; ++k) {
-        const int q = (rank + k) % world;
-        const int64_t len = seg_len(npk, sp, q, rb, re);
-        const int64_t lo = int64_t(r) * chp;
-        if (lo >= len) continue;
-        push_packs_g<T, VEC>(in, n, int64_t(q) * sp + rb + lo, min(chp, len - lo),
-                             S.ws[q] + hoff + int64_t(rank) * segb + (rb + lo) * 16, gtid, gnt);
-      }
-      gsync();
-      if (gtid < world && gtid != rank && r < nchunks(seg_len(npk, sp, gtid, rb, re), chp, s))
-        publish(&S.pad[gtid]->flag[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
-    }
-    return;
-  }
-
-  if (role == 1) {  // ----------------------------------------- reducers
-    const int64_t len = seg_len(npk, sp, rank, rb, re);
-    const int rows = nchunks(len, chp, s);
-    for (int r = 0; r < rows; ++r) {
-      if (gtid < world && gtid != rank) {
-        int e = wait_flag(&S.pad[rank]->flag[par][s][gtid], S.pad[rank], c.timeout_ns, c.err, epoch,
-                          sig, uint32_t(r + 1));
-        if (e) atomicCAS(s_err_p, 0, e);
-      }
-      gsync();
-      if (*verr) {
-        if (gtid == 0) raise_error(S.pad, world, c.err, *verr, epoch);
-        return;
-      }
-      const int64_t lo = int64_t(r) * chp, hi = min(len, lo + chp);
-      constexpr int RU = sizeof(T) == 2 ? 2 : 4;
-      for (int64_t i0 = rb + lo + gtid; i0 < rb + hi; i0 += RU * gnt) {
-        Pack<T> acc[RU];
-        uint4 v[RU];
-#pragma unroll
-        for (int u = 0; u < RU; ++u) {
-          const int64_t i = i0 + u * gnt;
-          if (i < rb + hi)
-            v[u] = rank == 0 ? load_pack<T, VEC>(in, int64_t(rank) * sp + i, n) : ld16_cg(ws + i * 16);
-        }
-#pragma unroll
-        for (int u = 0; u < RU; ++u) acc[u].from_raw(v[u]);
-        for (int q = 1; q < world; ++q) {
-#pragma unroll
-          for (int u = 0; u < RU; ++u) {
-            const int64_t i = i0 + u * gnt;
-            if (i < rb + hi)
-              v[u] = (q == rank) ? load_pack<T, VEC>(in, int64_t(rank) * sp + i, n)
-                                 : ld16_cg(ws + int64_t(q) * segb + i * 16);
-          }
-#pragma unroll
-          for (int u = 0; u < RU; ++u) acc[u].template fold<OP>(v[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < RU; ++u) {
-          const int64_t i = i0 + u * gnt;
-          if (i >= rb + hi) break;
-          const uint4 res = acc[u].to_raw();
-          for (int k = 1; k < world; ++k) {
-            const int q = (rank + k) % world;
-            st16(S.ws[q] + hoff + ag + int64_t(rank) * segb + i * 16, res);
-          }
-          store_pack<T, VEC>(out, int64_t(rank) * sp + i, n, res);
-        }
-      }
-      gsync();
-      if (gtid < world && gtid != rank)
-        publish(&S.pad[gtid]->flag2[par][s][rank], make_flag(epoch, sig, uint32_t(r + 1)));
-    }
-    return;
-  }
-
-  // ------------------------------------------------------------ gatherers
-  int rows = 0;
-  for (int q = 0; q < world; ++q)
-    if (q != rank) rows = max(rows, nchunks(seg_len(npk, sp, q, rb, re), chp, s));
-  for (int r = 0; r < rows; ++r) {
-    if (gtid < world && gtid != rank && r < nchunks(seg_len(npk, sp, gtid, rb, re), chp, s)) {
-      int e = wait_flag(&S.pad[rank]->flag2[par][s][gtid], S.pad[rank], c.timeout_ns, c.err, epoch,
-                        sig, uint32_t(r + 1));
-      if (e) atomicCAS(s_err_p, 0, e);
-    }
-    gsync();
-    if (*verr) {
-      if (gtid == 0) raise_error(S.pad, world, c.err, *verr, epoch);
-      return;
-    }
-    for (int k = 1; k < world; ++k) {
-      const int q = (rank + k) % world;
-      const int64_t len = seg_len(npk, sp, q, rb, re);
-      const int64_t lo = int64_t(r) * chp;
-      if (lo >= len) continue;
-      const int64_t hi = min(len, lo + chp);
-      const uint8_t* src = ws + ag + int64_t(q) * segb;
-      int64_t i = rb + lo + gtid;
-      for (; i + 3 * gnt < rb + hi; i += 4 * gnt) {
-        uint4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = ld16_cg(src + (i + u * gnt) * 16);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) store_pack<T, VEC>(out, int64_t(q) * sp + i + u * gnt, n, v[u]);
-      }
-      for (; i < rb + hi; i += gnt) store_pack<T, VEC>(out, int64_t(q) * sp + i, n, ld16_cg(src + i * 16));
-    }
-  }
-}
-
-template <typename T, int OP, bool VEC>
-__global__ void __launch_bounds__(kThreads, 2) k_ar_ws(DevComm c, const T* in, T* out, int64_t n, int64_t sp, int64_t segb, int64_t chp,
-            uint32_t sig) {
-  const uint32_t epoch = epoch_enter(c);
-  ar_ws_body<T, OP, VEC>(c, in, out, n, sp, segb, chp, epoch, sig);
   epoch_exit(c, epoch);
 }
 
@@ -1396,7 +1204,6 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
       const int64_t share = (sp + gp - 1) / gp;
       int64_t chp = (share + 3999) / 4000;  // <= 4000 chunks per share (12-bit flag step)
       if (chp < chunk_kb * 64) chp = chunk_kb * 64;  // KiB -> 16-byte packs
-      const int G = int(3 * gp);
       bool launched = false;
       if constexpr (kNvlsType && OP == MCRDL_SUM) {
         if (algo == MCRDL_ALGO_NVLS) {
@@ -1438,43 +1245,36 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
         static const int64_t tma_on = env_int("MCRDL_AR_TMA", 1);
         static const int64_t tma_ctas = env_int("MCRDL_AR_TMA_CTAS", 64);
         const bool big = m * int64_t(sizeof(T)) >= (int64_t(256) << 20);
-        // Warp-specialized kernel (one share per CTA, all roles per CTA):
-        // MCRDL_AR_KERNEL=1 selects it, 0 the CTA-role kernels below.
-        // Measured (tools/ws_ab.sh): p=2 +2%, p=4 -9% at 256 MiB -> default off.
-        static const int64_t ws_kernel = env_int("MCRDL_AR_KERNEL", 0);
-        // All-gather half: 1 = peers pull reduced segments, 0 = reducers push.
-        static const int ag_pull = int(env_int("MCRDL_AR_AG_PULL", 0));
-        int64_t gw = (sp * 16 + (32 << 10) - 1) / (32 << 10);
-        gw = std::max<int64_t>(1, std::min<int64_t>(gw, std::min<int64_t>(2 * c->num_sms, kMaxBlocks)));
-        const int64_t sharew = (sp + gw - 1) / gw;
-        int64_t chpw = (sharew + 3999) / 4000;
-        if (chpw < chunk_kb * 64) chpw = chunk_kb * 64;
-        if (ws_kernel == 1 && root < 0) {
-          if (vec)
-            k_ar_ws<T, OP, true><<<int(gw), kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, chpw,
-                                                                   sig);
-          else
-            k_ar_ws<T, OP, false><<<int(gw), kThreads, 0, stream>>>(c->dc, ip, op, m, sp, segb, chpw,
-                                                                    sig);
-        } else if (vec && (tma_on == 2 || (tma_on == 1 && big))) {
+        {
+          // Share geometry (shares, chunk) comes only from values every rank
+          // agrees on (size, SM budget, env); buffer alignment only picks the
+          // sender flavour. TMA geometry: few single-thread bulk-copy sender
+          // CTAs leave room for more reducer/gatherer shares.
+          const bool tma_geo = tma_on == 2 || (tma_on == 1 && big);
           const int gs = int(std::min<int64_t>(gp, tma_ctas));
-          int64_t gpt = gp;
-          const int64_t cap = (2 * c->num_sms - gs) / 2;  // gs + 2*gp <= 2 CTAs/SM
-          if (gp_env <= 0 && gpt < cap) {
-            gpt = std::min<int64_t>(cap, (sp * 16 + (32 << 10) - 1) / (32 << 10));
-            if (gpt < 1) gpt = 1;
+          int64_t shares = gp, chs = chp;
+          if (tma_geo) {
+            const int64_t cap = (2 * c->num_sms - gs) / 2;  // gs + 2*gp <= 2 CTAs/SM
+            if (gp_env <= 0 && shares < cap) {
+              shares = std::min<int64_t>(cap, (sp * 16 + (32 << 10) - 1) / (32 << 10));
+              if (shares < 1) shares = 1;
+            }
+            chs = ((sp + shares - 1) / shares + 3999) / 4000;
+            if (chs < chunk_kb * 64) chs = chunk_kb * 64;
           }
-          const int64_t sharet = (sp + gpt - 1) / gpt;
-          int64_t chpt = (sharet + 3999) / 4000;
-          if (chpt < chunk_kb * 64) chpt = chunk_kb * 64;
-          k_ar_pipe<T, OP, true, true><<<int(gs + 2 * gpt), kThreads, 0, stream>>>(
-              c->dc, ip, op, m, sp, segb, int(gpt), gs, chpt, ag_pull, root, sig);
-        } else if (vec) {
-          k_ar_pipe<T, OP, true, false><<<G, kThreads, 0, stream>>>(
-              c->dc, ip, op, m, sp, segb, int(gp), int(gp), chp, ag_pull, root, sig);
-        } else {
-          k_ar_pipe<T, OP, false, false><<<G, kThreads, 0, stream>>>(
-              c->dc, ip, op, m, sp, segb, int(gp), int(gp), chp, ag_pull, root, sig);
+          // Any geometry disagreement (env knobs) fails as ORDER_MISMATCH
+          // instead of folding bytes that have not landed.
+          const uint32_t gsig = mix32(mix32(sig, uint64_t(shares)), uint64_t(chs)) & ~kSigCodecBit;
+          if (tma_geo && vec) {
+            k_ar_pipe<T, OP, true, true><<<int(gs + 2 * shares), kThreads, 0, stream>>>(
+                c->dc, ip, op, m, sp, segb, int(shares), gs, chs, root, gsig);
+          } else if (vec) {
+            k_ar_pipe<T, OP, true, false><<<int(3 * shares), kThreads, 0, stream>>>(
+                c->dc, ip, op, m, sp, segb, int(shares), int(shares), chs, root, gsig);
+          } else {
+            k_ar_pipe<T, OP, false, false><<<int(3 * shares), kThreads, 0, stream>>>(
+                c->dc, ip, op, m, sp, segb, int(shares), int(shares), chs, root, gsig);
+          }
         }
       }
     }
@@ -1527,7 +1327,7 @@ static mcrdl_status_t rs_typed(mcrdl_comm* c, const T* in, T* out, int64_t m, ui
   if (chp < 16384) chp = 16384;
   // senders + reducers only (reduce_scatter has no all-gather role)
   k_ar_pipe<T, OP, true, false><<<int(2 * gp), kThreads, 0, stream>>>(
-      c->dc, in, out, int64_t(world) * m, sp, segb, int(gp), int(gp), chp, 0, -1, sig, out, m);
+      c->dc, in, out, int64_t(world) * m, sp, segb, int(gp), int(gp), chp, -1, sig, out, m);
   count_launch();
   MCRDL_CUDA_CHECK(cudaGetLastError());
   return MCRDL_OK;

@@ -151,10 +151,10 @@ static socklen_t sock_name(sockaddr_un* a, uint64_t jobid, int rank) {
   return socklen_t(offsetof(sockaddr_un, sun_path) + 1 + n);
 }
 
-// Messages that arrived early for a later exchange tag: (tag, rank) -> fd.
-static std::map<std::pair<int, int>, int> g_stash;
-static std::mutex g_stash_mu;
-static int g_fd_tag = 0;
+// Messages that arrived early for a later exchange tag live in the comm
+// (c->fd_stash: (tag, rank) -> fd) and tags count per comm (c->fd_tag): several
+// communicators of one process (ranks sharing a GPU as threads, or several
+// backends) must not consume each other's tags.
 
 static mcrdl_status_t send_fd(uint64_t jobid, int to, int from, int tag, int fd, double timeout_s) {
   sockaddr_un addr;
@@ -218,7 +218,7 @@ static mcrdl_status_t recv_one_fd(int listen_fd, double timeout_s, FdMsg* m, int
 
 // Every rank sends `my_fd` to every peer and collects one fd per peer.
 static mcrdl_status_t exchange_fds(mcrdl_comm* c, int my_fd, int peer_fds[kMaxRanks]) {
-  const int tag = ++g_fd_tag;
+  const int tag = ++c->fd_tag;
   const double tmo = double(c->timeout_ns) * 1e-9 + 30.0;
   for (int r = 0; r < c->world; ++r) peer_fds[r] = -1;
   peer_fds[c->rank] = my_fd;
@@ -228,15 +228,12 @@ static mcrdl_status_t exchange_fds(mcrdl_comm* c, int my_fd, int peer_fds[kMaxRa
     if (st != MCRDL_OK) return st;
   }
   int have = 0;
-  {
-    std::lock_guard<std::mutex> lk(g_stash_mu);
-    for (int r = 0; r < c->world; ++r) {
-      auto it = g_stash.find({tag, r});
-      if (it != g_stash.end()) {
-        peer_fds[r] = it->second;
-        g_stash.erase(it);
-        ++have;
-      }
+  for (int r = 0; r < c->world; ++r) {
+    auto it = c->fd_stash.find({tag, r});
+    if (it != c->fd_stash.end()) {
+      peer_fds[r] = it->second;
+      c->fd_stash.erase(it);
+      ++have;
     }
   }
   while (have < c->world - 1) {
@@ -248,8 +245,7 @@ static mcrdl_status_t exchange_fds(mcrdl_comm* c, int my_fd, int peer_fds[kMaxRa
       peer_fds[m.rank] = fd;
       ++have;
     } else {
-      std::lock_guard<std::mutex> lk(g_stash_mu);
-      g_stash[{m.tag, m.rank}] = fd;
+      c->fd_stash[{m.tag, m.rank}] = fd;
     }
   }
   return MCRDL_OK;
@@ -341,7 +337,7 @@ static mcrdl_status_t alloc_region(mcrdl_comm* c, uint64_t bytes, Region* rg) {
 
 // Rank 0 hands one fd to every peer (the multicast object handle).
 static mcrdl_status_t bcast_fd(mcrdl_comm* c, int fd, int* out_fd) {
-  const int tag = ++g_fd_tag;
+  const int tag = ++c->fd_tag;
   const double tmo = double(c->timeout_ns) * 1e-9 + 30.0;
   if (c->rank == 0) {
     for (int r = 1; r < c->world; ++r) {
@@ -352,11 +348,10 @@ static mcrdl_status_t bcast_fd(mcrdl_comm* c, int fd, int* out_fd) {
     return MCRDL_OK;
   }
   {
-    std::lock_guard<std::mutex> lk(g_stash_mu);
-    auto it = g_stash.find({tag, 0});
-    if (it != g_stash.end()) {
+    auto it = c->fd_stash.find({tag, 0});
+    if (it != c->fd_stash.end()) {
       *out_fd = it->second;
-      g_stash.erase(it);
+      c->fd_stash.erase(it);
       return MCRDL_OK;
     }
   }
@@ -369,8 +364,7 @@ static mcrdl_status_t bcast_fd(mcrdl_comm* c, int fd, int* out_fd) {
       *out_fd = got;
       return MCRDL_OK;
     }
-    std::lock_guard<std::mutex> lk(g_stash_mu);
-    g_stash[{m.tag, m.rank}] = got;
+    c->fd_stash[{m.tag, m.rank}] = got;
   }
 }
 
@@ -495,10 +489,11 @@ static mcrdl_status_t setup_nvls(mcrdl_comm* c, uint64_t bytes) {
   }
   if (ok) {  // multicast flag words at the end of each half start at 0
     for (int h = 0; h < 2; ++h)
-      if (cudaMemset(reinterpret_cast<uint8_t*>(nv.uc_ptr) + (h + 1) * (bytes / 2) - kNvlsFlagBytes,
-                     0, kNvlsFlagBytes) != cudaSuccess)
+      if (cudaMemsetAsync(reinterpret_cast<uint8_t*>(nv.uc_ptr) + (h + 1) * (bytes / 2) -
+                              kNvlsFlagBytes,
+                          0, kNvlsFlagBytes, c->aux) != cudaSuccess)
         ok = 0;
-    if (cudaDeviceSynchronize() != cudaSuccess) ok = 0;
+    if (cudaStreamSynchronize(c->aux) != cudaSuccess) ok = 0;
   }
   if ((st = host_allgather(c, &ok, oks, sizeof(int))) != MCRDL_OK) return st;
   for (int r = 0; r < c->world; ++r) ok &= oks[r];
@@ -608,18 +603,59 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   c->allgather = allgather;
   c->ag_ctx = ctx;
   if (timeout_secs > 0) c->timeout_ns = uint64_t(timeout_secs * 1e9);
-  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  int dev_sms = 0;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   auto fail = [&](mcrdl_status_t s) {
     mcrdl_comm_destroy(c);
     return s;
   };
+  MCRDL_CUDA_CHECK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+  for (auto& x : c->xfer) MCRDL_CUDA_CHECK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
 
-  // Job id from rank 0 (fresh random per init) names the sockets.
+  // Job id from rank 0 (fresh random per init) names the sockets; the device
+  // UUIDs tell which ranks share a GPU.
+  struct Hello {
+    uint64_t id;
+    unsigned char uuid[16];
+    int32_t sms;
+    int32_t pad;
+  } mine{}, all[kMaxRanks];
   std::random_device rd;
-  uint64_t mine = (uint64_t(rd()) << 32) ^ rd() ^ uint64_t(getpid());
-  uint64_t ids[kMaxRanks];
-  if ((st = host_allgather(c, &mine, ids, sizeof(uint64_t))) != MCRDL_OK) return fail(st);
-  c->jobid = ids[0];
+  mine.id = (uint64_t(rd()) << 32) ^ rd() ^ uint64_t(getpid());
+  {
+    cudaDeviceProp prop;
+    MCRDL_CUDA_CHECK(cudaGetDeviceProperties(&prop, cuda_device));
+    memcpy(mine.uuid, prop.uuid.bytes, 16);
+  }
+  // MCRDL_MAX_SMS: SM budget for this rank's collectives (the rest stays free
+  // for overlapped compute); co-located ranks split the device between them.
+  mine.sms = dev_sms;
+  if (const int64_t cap = env_int("MCRDL_MAX_SMS", 0); cap > 0 && cap < mine.sms) mine.sms = int32_t(cap);
+  if ((st = host_allgather(c, &mine, all, sizeof(Hello))) != MCRDL_OK) return fail(st);
+  c->jobid = all[0].id;
+  int budget = mine.sms;
+  for (int q = 0; q < world; ++q) {
+    int same = 0;
+    for (int k = 0; k < world; ++k) same += memcmp(all[q].uuid, all[k].uuid, 16) == 0;
+    c->ranks_per_device = std::max(c->ranks_per_device, same);
+    budget = std::min<int>(budget, all[q].sms);
+  }
+  // Co-located ranks: every rank's grids (at most 2 CTAs per budgeted SM, up
+  // to two chains in flight per rank) must be resident at once, or a spinning
+  // grid would wait for a peer grid that cannot be scheduled.
+  if (c->ranks_per_device > 1) budget = std::min(budget, dev_sms / (2 * c->ranks_per_device));
+  c->num_sms = std::max(1, budget);
+  if (c->ranks_per_device > 1) {
+    // Lazy kernel loading waits for the context to idle: a co-located rank's
+    // first launch of a kernel would wait on a peer kernel spinning for it.
+    PFN_cuModuleGetLoadingMode getmode = nullptr;
+    CUmoduleLoadingMode mode = CU_MODULE_EAGER_LOADING;
+    if (resolve("cuModuleGetLoadingMode", &getmode) && getmode(&mode) == CUDA_SUCCESS &&
+        mode != CU_MODULE_EAGER_LOADING && rank == 0)
+      fprintf(stderr, "[mcrdl] warning: %d ranks share a GPU under lazy module loading; set "
+                      "CUDA_MODULE_LOADING=EAGER or first launches can stall until the timeout\n",
+              c->ranks_per_device);
+  }
 
   if (world > 1) {
     c->listen_fd = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
@@ -650,12 +686,18 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
       (uint64_t(mbox) + (mbox > 0 ? uint64_t(kP2PLLSenderBytes) : 0)) * uint64_t(world);
   if ((st = alloc_region(c, kPadBytes + workspace_bytes + p2p_bytes, &c->base)) != MCRDL_OK)
     return fail(st);
-  MCRDL_CUDA_CHECK(cudaMemset(reinterpret_cast<void*>(c->base.ptr[rank]), 0, kPadBytes));
-  MCRDL_CUDA_CHECK(cudaDeviceSynchronize());
+  // Setup memsets run on the comm's private stream and are waited for on
+  // that stream only: a device-wide sync could wait on spinning kernels of
+  // co-located ranks whose peers have not launched yet.
+  MCRDL_CUDA_CHECK(cudaMemsetAsync(reinterpret_cast<void*>(c->base.ptr[rank]), 0, kPadBytes, c->aux));
+  MCRDL_CUDA_CHECK(cudaStreamSynchronize(c->aux));
 
   // NVLS buffer: half the workspace size by default; MCRDL_NVLS_BYTES=0 disables.
   uint64_t nvls_bytes = workspace_bytes / 2;
   if (const char* e = getenv("MCRDL_NVLS_BYTES")) nvls_bytes = strtoull(e, nullptr, 10);
+  // A multicast object spans distinct GPUs: none for co-located ranks (agreed:
+  // every rank computed ranks_per_device from the same UUID table).
+  if (c->ranks_per_device > 1) nvls_bytes = 0;
   if (nvls_bytes > 0 && (st = setup_nvls(c, nvls_bytes)) != MCRDL_OK) return fail(st);
 
   MCRDL_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(int),
@@ -691,6 +733,10 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   }
   // Nobody may signal into a pad before its owner zeroed it.
   if ((st = host_barrier(c)) != MCRDL_OK) return fail(st);
+  if (env_int("MCRDL_DEBUG", 0))
+    fprintf(stderr, "[mcrdl] comm %p rank %d/%d dev %d sms %d co-located %d pad %p nvls %d\n",
+            (void*)c, rank, world, cuda_device, c->num_sms, c->ranks_per_device,
+            (void*)c->base.ptr[rank], int(c->nvls.ok));
   *out = c;
   return MCRDL_OK;
 }
@@ -708,6 +754,10 @@ mcrdl_status_t mcrdl_comm_destroy(mcrdl_comm* c) {
     if (ch.ev) cudaEventDestroy(ch.ev);
   if (c->trace_host) cudaFreeHost(c->trace_host);
   if (c->oplog_host) cudaFreeHost(c->oplog_host);
+  if (c->aux) cudaStreamDestroy(c->aux);
+  for (auto& x : c->xfer)
+    if (x) cudaStreamDestroy(x);
+  for (auto& kv : c->fd_stash) close(kv.second);
   if (c->listen_fd >= 0) close(c->listen_fd);
   delete c;
   return MCRDL_OK;
@@ -746,9 +796,17 @@ mcrdl_status_t mcrdl_comm_caps(const mcrdl_comm* c, mcrdl_caps_t* caps) {
   caps->device = c->device;
   caps->num_sms = c->num_sms;
   caps->nvls_supported = c->nvls.ok ? 1 : 0;
+  caps->ranks_per_device = c->ranks_per_device;
   caps->workspace_bytes = c->ws_bytes;
   caps->max_oneshot_bytes = uint64_t(c->dc.half_bytes) / uint64_t(c->world) / 256 * 256;
   caps->max_twoshot_chunk = uint64_t(c->dc.half_bytes) / 2 / 256 * 256;
+  return MCRDL_OK;
+}
+
+mcrdl_status_t mcrdl_comm_stream(const mcrdl_comm* c, int which, void** stream) {
+  if (c == nullptr || stream == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL argument");
+  if (which < 0 || which > 2) return set_error(MCRDL_ERR_VALIDATION, "stream index %d", which);
+  *stream = reinterpret_cast<void*>(which == 0 ? c->aux : c->xfer[which - 1]);
   return MCRDL_OK;
 }
 
@@ -784,12 +842,12 @@ mcrdl_status_t mcrdl_symm_alloc(mcrdl_comm* c, uint64_t bytes, void** local_ptr)
     unmap_region(c, rg);
     return st;
   }
-  MCRDL_CUDA_CHECK(cudaMemset(reinterpret_cast<void*>(rg.ptr[c->rank]), 0, rg.bytes));
+  MCRDL_CUDA_CHECK(cudaMemsetAsync(reinterpret_cast<void*>(rg.ptr[c->rank]), 0, rg.bytes, c->aux));
   if (c->nvls.ok && mg > 0 && (st = bind_multicast(c, &rg)) != MCRDL_OK) {
     unmap_region(c, rg);
     return st;
   }
-  MCRDL_CUDA_CHECK(cudaDeviceSynchronize());
+  MCRDL_CUDA_CHECK(cudaStreamSynchronize(c->aux));
   c->symm.push_back(rg);
   *local_ptr = reinterpret_cast<void*>(rg.ptr[c->rank]);
   return MCRDL_OK;

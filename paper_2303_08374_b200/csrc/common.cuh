@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "../../include/mcrdl_nvl.h"
 
@@ -224,7 +225,9 @@ __device__ __forceinline__ void epoch_exit(const DevComm& c, uint32_t epoch) {
 static __device__ __noinline__ void raise_error(Pad* const* pads, int world, int* err, int code,
                                                 uint32_t epoch) {
   const int par = epoch & 1;
-  atomicCAS(err, 0, code);
+  if (atomicCAS(err, 0, code) == 0)
+    printf("[mcrdl] raise_error: code %d epoch %u (pad %p, block %d)\n", code, epoch,
+           (const void*)pads[0], int(blockIdx.x));
   for (int r = 0; r < world; ++r) {
     st_relaxed_sys(&pads[r]->abort_word[par][1], uint64_t(code));
     __threadfence_system();
@@ -275,6 +278,11 @@ static __device__ __noinline__ int wait_flag(const uint64_t* p, const Pad* me, u
       if (start == 0) {
         start = now;
       } else if (now - start > timeout_ns) {
+        // one diagnostic line per timed-out waiter (exceptional path only)
+        printf("[mcrdl] flag timeout: pad %p word %p want epoch %u sig %05x step>=%u, saw %016llx "
+               "(block %d thread %d)\n",
+               (const void*)me, (const void*)p, epoch, sig & 0xFFFFFu, step & 0xFFFu,
+               (unsigned long long)v, int(blockIdx.x), int(threadIdx.x));
         return MCRDL_ERR_TIMEOUT;
       }
     }
@@ -296,6 +304,9 @@ static __device__ __noinline__ int wait_geq(const uint64_t* p, const Pad* me, ui
       if (start == 0) {
         start = now;
       } else if (now - start > timeout_ns) {
+        printf("[mcrdl] counter timeout: pad %p word %p want >= %llu, saw %llu (block %d thread %d)\n",
+               (const void*)me, (const void*)p, (unsigned long long)target,
+               (unsigned long long)ld_relaxed_sys(p), int(blockIdx.x), int(threadIdx.x));
         return MCRDL_ERR_TIMEOUT;
       }
     }

@@ -7,7 +7,9 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdint>
+#include <map>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/mcrdl_nvl.h"
@@ -48,7 +50,20 @@ struct mcrdl_comm {
   int rank = 0;
   int world = 1;
   int device = 0;
+  // SM budget every launch is sized from (grids stay <= 2 CTAs per budgeted
+  // SM). The device's SM count, divided between the ranks that share this
+  // GPU (co-located ranks: their spinning grids must all be resident at once),
+  // capped by MCRDL_MAX_SMS (leave SMs to overlapped compute), and agreed by
+  // every rank (min) because launch geometry must match across ranks.
   int num_sms = 0;
+  int ranks_per_device = 1;  // max ranks sharing one physical GPU in this comm
+  // The comm's own non-blocking stream: setup memsets, and the host layer's
+  // lane for async posts (mcrdl_comm_stream). One per comm, never pooled, so
+  // two communicators (e.g. co-located ranks) never share a stream.
+  cudaStream_t aux = nullptr;
+  cudaStream_t xfer[2] = {nullptr, nullptr};  // H2D / D2H staging (pipelined host posts)
+  int fd_tag = 0;                              // fd-exchange round counter
+  std::map<std::pair<int, int>, int> fd_stash; // (tag, rank) -> early fd
   mcrdl_allgather_fn allgather = nullptr;
   void* ag_ctx = nullptr;
   uint64_t jobid = 0;

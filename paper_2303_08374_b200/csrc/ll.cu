@@ -112,7 +112,7 @@ mcrdl_status_t launch_ar_ll(mcrdl_comm* c, const T* in, T* out, int64_t n,
   if (nu * 8 > kLLMaxPayload)
     return set_error(MCRDL_ERR_INTERNAL, "LL all_reduce above the LL slot size");
   int64_t g = (nu + kLLThreads - 1) / kLLThreads;
-  g = std::max<int64_t>(1, std::min<int64_t>(g, 32));
+  g = std::max<int64_t>(1, std::min<int64_t>(g, std::min(32, 4 * c->num_sms)));
   k_ar_ll<T, OP><<<int(g), kLLThreads, 0, stream>>>(c->dc, in, out, n, sig);
   count_launch();
   MCRDL_CUDA_CHECK(cudaGetLastError());
@@ -251,7 +251,7 @@ bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, int64_t ll_max, cuda
   a.sig_base = sp.sig_base;
   int64_t g = (mx / 8 + kLLThreads * 2 - 1) / (kLLThreads * 2);
   g = std::max<int64_t>(g, (sp.sbytes[c->rank] + (256 << 10) - 1) >> 18);
-  g = std::max<int64_t>(1, std::min<int64_t>(g, 64));
+  g = std::max<int64_t>(1, std::min<int64_t>(g, std::min(64, 4 * c->num_sms)));
   k_exchange_ll<<<int(g), kLLThreads, 0, stream>>>(c->dc, a);
   count_launch();
   cudaError_t e = cudaGetLastError();

@@ -60,6 +60,9 @@ static __device__ __noinline__ bool poll_ll(const void* p, uint32_t epoch, const
       const uint64_t now = globaltimer_ns();
       if (start == 0) start = now;
       else if (now - start > timeout_ns) {
+        printf("[mcrdl] LL timeout: pad %p line %p want epoch %u, saw {%08x %08x %08x %08x} "
+               "(block %d thread %d)\n",
+               (const void*)me, p, epoch, v.x, v.y, v.z, v.w, int(blockIdx.x), int(threadIdx.x));
         *err = MCRDL_ERR_TIMEOUT;
         return false;
       }

@@ -325,7 +325,8 @@ mcrdl_status_t p2p_launch(mcrdl_comm* c, void* buf, uint64_t bytes, int peer, bo
   if (G < 1) G = 1;
   Pad* peer_pad = c->dc.pad[peer];
   if (bytes <= uint64_t(kP2PLLMax)) {  // small: LL lines, 8 KiB of payload per CTA
-    const int gl = int(std::max<uint64_t>(1, (bytes + kP2PLLCtaBytes - 1) / kP2PLLCtaBytes));
+    const int gl = int(std::min<uint64_t>(std::max<uint64_t>(1, (bytes + kP2PLLCtaBytes - 1) / kP2PLLCtaBytes),
+                                          uint64_t(2 * c->num_sms)));
     if (is_send)
       k_send_ll<<<gl, kP2PThreads, 0, stream>>>(c->dc, c->dc.ws[peer],
                                                 static_cast<const uint8_t*>(buf), int64_t(bytes),

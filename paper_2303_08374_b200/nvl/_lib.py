@@ -23,7 +23,7 @@ ALLGATHER_FN = CFUNCTYPE(c_int, c_void_p, c_void_p, c_void_p, c_size_t)
 class Caps(Structure):
     _fields_ = [
         ("rank", c_int), ("world", c_int), ("device", c_int), ("num_sms", c_int),
-        ("nvls_supported", c_int), ("reserved0", c_int),
+        ("nvls_supported", c_int), ("ranks_per_device", c_int),
         ("workspace_bytes", c_uint64), ("max_oneshot_bytes", c_uint64),
         ("max_twoshot_chunk", c_uint64),
     ]
@@ -38,6 +38,7 @@ SIGNATURES = {
     "mcrdl_comm_destroy": (c_int, [_P]),
     "mcrdl_comm_caps": (c_int, [_P, POINTER(Caps)]),
     "mcrdl_comm_status": (c_int, [_P]),
+    "mcrdl_comm_stream": (c_int, [_P, c_int, POINTER(c_void_p)]),
     "mcrdl_comm_log_id": (c_uint64, [_P]),
     "mcrdl_comm_op_time": (c_int, [_P, c_uint64, c_uint64, _I64P]),
     "mcrdl_symm_alloc": (c_int, [_P, c_uint64, POINTER(c_void_p)]),

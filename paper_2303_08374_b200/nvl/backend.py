@@ -60,6 +60,13 @@ class NvlComm:
     def status(self) -> None:
         _lib.check(self.lib.mcrdl_comm_status(self.handle))
 
+    def stream(self, which: int):
+        """One of the communicator's own CUDA streams as a torch stream
+        (0: lane, 1: H2D staging, 2: D2H staging)."""
+        raw = c_void_p()
+        _lib.check(self.lib.mcrdl_comm_stream(self.handle, int(which), byref(raw)))
+        return torch.cuda.ExternalStream(int(raw.value), device=self.device)
+
     def symm_alloc(self, nbytes: int) -> int:
         """Collective: a peer-mapped (and, with NVLS, multicast-bound) device
         allocation of `nbytes` on every rank; returns this rank's pointer."""
@@ -246,7 +253,6 @@ class NvlBackendInstance:
             dev = runtime.rank % max(n_dev, 1)
         self.device = int(dev)
         torch.cuda.set_device(self.device)
-        self.stream = torch.cuda.Stream(device=self.device)
         boot = None
         if runtime.world_size > 1:
             store = runtime._control_store(config)
@@ -255,6 +261,9 @@ class NvlBackendInstance:
         ws = config.workspace_bytes or runtime.default_workspace_bytes
         self.comm = NvlComm(runtime.rank, runtime.world_size, self.device, boot, ws,
                             runtime.timeout)
+        # Lane = the communicator's own stream (not one from torch's
+        # round-robin pool, which hands the same stream to several callers).
+        self.stream = self.comm.stream(0)
 
     # ------------------------------------------------------------ properties
     @property
@@ -316,6 +325,7 @@ class NvlBackendInstance:
             raise BackendFinalized(f"backend {self.name!r} is {self.state}")
         with self._lock:
             self._assign_seq(request)
+            self._pre_launch(request)
             lib, c = self.comm.lib, self.comm.handle
             log = self.runtime.log_ops
             if log:
@@ -363,6 +373,7 @@ class NvlBackendInstance:
         handle = WorkHandle(self.name, request)
         with self._lock:
             self._assign_seq(request)
+            self._pre_launch(request)  # before any stream work of this op
             handle.mark_in_progress()
             self._reap()
             if self._pipelined_ok(request):
@@ -409,9 +420,12 @@ class NvlBackendInstance:
         step = ((n + k - 1) // k + 63) // 64 * 64
         h_in, h_out = req.input.array, req.output.array
         lane = self.stream
+        # the first H2D chunk reads h_in: order it after the caller's work
+        # (e.g. a non_blocking D2H that fills the pinned tensor)
+        lane.wait_stream(torch.cuda.current_stream(self.device))
         if getattr(self, "_up", None) is None:
-            self._up = torch.cuda.Stream(device=self.device)
-            self._down = torch.cuda.Stream(device=self.device)
+            self._up = self.comm.stream(1)
+            self._down = self.comm.stream(2)
         up, down = self._up, self._down
         with torch.cuda.stream(lane):
             d = torch.empty(n, dtype=dt.torch_dtype, device=self.device)
@@ -458,6 +472,7 @@ class NvlBackendInstance:
         with self._lock:
             flush_request.seq = self._seq
             self._seq += 1
+            self._pre_launch(flush_request)  # before any stream work of this op
             handle.mark_in_progress()
             lane = self.stream
             for ev in ready_events:
@@ -593,6 +608,18 @@ class NvlBackendInstance:
         self.comm.destroy()
 
     # ---------------------------------------------------------------- launch
+    def _pre_launch(self, req: CommRequest, sub: int = 0) -> None:
+        """Runtime.launch_hook (tests): called with (backend, seq, sub) right
+        before a collective's C-ABI call. Co-located thread-rank tests use it
+        to launch every rank's kernel of one op together, so that a device-
+        synchronizing host call (cudaMalloc/cudaHostAlloc in torch's
+        allocators, lazy module loads) in one rank never waits on a peer
+        kernel that spins for an op this rank has not launched yet."""
+        hook = self.runtime.launch_hook
+        if (hook is not None and req.kind not in P2P_KINDS and self.world_size > 1
+                and not torch.cuda.is_current_stream_capturing()):  # captures launch nothing
+            hook((self.name, req.seq, sub))
+
     def _launch(self, req: CommRequest, st: _Staging, s: int) -> None:
         lib, c = self.comm.lib, self.comm.handle
         kind, p, rank, seq = req.kind, self.world_size, self.rank, req.seq

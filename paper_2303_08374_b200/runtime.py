@@ -109,6 +109,10 @@ class Runtime:
         self._fusion: Optional[FusionManager] = None
         self._store = None
         self._init_generation = 0
+        # Test hook: callable((backend, seq, sub)) run right before every
+        # collective's native launch (co-located thread-rank tests launch each
+        # op's kernels together; tests/gpu_worker.py). None in production.
+        self.launch_hook = None
         path = os.environ.get(ENV_TUNING_TABLE)
         if path:
             self.tuning_table = dispatch.load_table(path)

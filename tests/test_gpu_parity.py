@@ -1,10 +1,16 @@
 """GPU parity: the nvlink backend (sm_100a kernels through the C ABI, driven
 by the public Runtime API) against the CPU oracle and the reference's golden
-dumps, one process per GPU. Every scenario checks every rank's output:
-bit-exact for movement, integer and (ascending-fold) float reductions.
+dumps. Every scenario checks every rank's output: bit-exact for movement,
+integer and (ascending-fold) float reductions.
 
-World sizes run only when that many GPUs are visible (never more ranks than
-GPUs: spinning kernels must not share a GPU)."""
+Two layouts:
+* one process per GPU (production): world sizes run when that many GPUs are
+  visible;
+* co-located: p thread-ranks of one process on ONE GPU (the reference's
+  thread-world layout). The communicator sees the shared device,
+  splits the SMs so every rank's spinning grids are resident together and has
+  no NVLS; every other kernel and the whole flag protocol run as in
+  production, so p = 2, 4, 8 parity runs on a single B200."""
 
 import pytest
 
@@ -42,6 +48,16 @@ def test_parity_all_scenarios(world):
     _assert_ok(run_world(world, SCENARIOS, timeout=900.0))
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_parity_colocated(world):
+    if _ngpu() < 1:
+        pytest.skip("no GPU")
+    reports = run_world(world, SCENARIOS, timeout=1500.0, colocated=True)
+    _assert_ok(reports)
+    assert all(rep.get("colocated") == world for rep in reports), \
+        [rep.get("colocated") for rep in reports]
+
+
 def test_smoke_entry_point():
     if _ngpu() < 1:
         pytest.skip("no GPU")
@@ -54,6 +70,6 @@ def test_host_buffers_are_staged_through_the_device():
     """No CPU fallback: reference-style numpy Buffers on an nvlink backend are
     staged to the device and reduced by the sm_100a kernels (the partner.py
     known answers, p = 2)."""
-    if _ngpu() < 2:
-        pytest.skip("needs 2 GPUs")
-    _assert_ok(run_world(2, ["host_buffers"], timeout=300.0))
+    if _ngpu() < 1:
+        pytest.skip("no GPU")
+    _assert_ok(run_world(2, ["host_buffers"], timeout=300.0, colocated=_ngpu() < 2))
