@@ -6,8 +6,11 @@ all_reduce (sum, fp32, out of place) of S = 256 MiB per rank through the
 public API (Runtime.post on an nvlink backend), configs[1]'s >= 64 MB point.
 
   value  = whole-job bus bytes / time = N * busbw, busbw = 2(N-1)/N * S / t
-           (nccl-tests definition). At N = 1 there is no bus: the step is the
-           local-copy floor and its bytes are 2*S (read + write).
+           (nccl-tests definition), the same definition at every N. At N = 1
+           there are no peers: the all_reduce is a local copy and its bus
+           bytes are taken as S (each element delivered once); the HBM view
+           of that copy (2*S read + write vs the HBM peak) is reported
+           separately as config.local_copy_floor_gbs and in `roofline`.
   e2e    = the same metric through the same API with HOST (pinned) buffers:
            H2D of the input, the collective, D2H of the result, per step.
   roofline: dominant kernel (k_ar_pipe for N > 1, k_copy for N = 1),
@@ -15,10 +18,13 @@ public API (Runtime.post on an nvlink backend), configs[1]'s >= 64 MB point.
            the launching stream) vs NVLink 900 GB/s/direction (N > 1) or
            the measured HBM copy peak (N = 1).
   cpu_baseline: the reference package itself (baseline/_ref, pure Python +
-           numpy, thread world of N ranks) on a bounded sample, rank 0, N=1.
+           numpy, thread world of N ranks, the SAME S) on a bounded number of
+           steps, rank 0, at every N.
 
-  --impl reference  times the reference's own CPU implementation (same
-           metric and config, bounded sample) on rank 0; other ranks exit.
+  --impl reference  times the reference's own CPU implementation on the same
+           metric, config (S per rank, N thread-ranks) and --steps/--warmup
+           (capped only if the estimate exceeds a few minutes, then stated);
+           rank 0 runs it, other ranks exit.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
        (N > 1: launched under torch.distributed.run, one process per GPU)
@@ -63,8 +69,9 @@ def measured_peaks():
 
 
 def bus_bytes(n: int, size: int) -> float:
-    """Per-rank bus bytes of one all_reduce (p = 1: local copy read+write)."""
-    return 2.0 * size if n == 1 else 2.0 * (n - 1) / n * size
+    """Per-rank bus bytes of one all_reduce: 2(n-1)/n * S (nccl-tests busbw);
+    n = 1 (no peers, a local copy): S, each element delivered once."""
+    return float(size) if n == 1 else 2.0 * (n - 1) / n * size
 
 
 # --------------------------------------------------------------- clocks
@@ -181,30 +188,44 @@ def cpu_info():
     return os.cpu_count(), model
 
 
+def reference_line_cpu(n: int, size: int, t: float, steps: int, note: str = "") -> dict:
+    cores, model = cpu_info()
+    return {"value": n * bus_bytes(n, size) / t / 1e9, "unit": "GB/s", "cores": n,
+            "nproc": cores, "cpu_model": model, "kind": "reference",
+            "sample": f"{steps} steps of all_reduce sum f32 {size // MIB} MiB per rank x {n} "
+                      f"thread-ranks of the reference (baseline/_ref mcrdl, inproc transport, "
+                      f"default ring policy, tuner.py:151-214 timing; one Python process, GIL)"
+                      f"{note}"}
+
+
 def run_reference(args) -> int:
     rank = int(os.environ.get("RANK", "0"))
     n = args.gpus
     if rank != 0:
         return 0
-    # Bounded sample: S_ref per rank sized so the run stays within minutes.
-    size = min(args.size_mib, 32 if n <= 2 else 16) * MIB
-    steps = max(3, min(args.steps, 10))
-    warmup = max(1, min(args.warmup, 3))
+    # Same config as the native arm: S per rank, N ranks, --steps/--warmup.
+    size = args.size_mib * MIB
+    steps, warmup = args.steps, args.warmup
+    t_probe, _ = reference_allreduce(n, size, 1, 0)
+    budget = float(os.environ.get("MCRDL_REF_BUDGET_S", "240"))
+    note = ""
+    if t_probe * (steps + warmup) > budget:  # keep the run within minutes
+        steps = max(3, int(budget / t_probe) - warmup)
+        note = f"; steps capped to {steps} (probe {t_probe:.2f} s/step, budget {budget:.0f} s)"
     t, _ = reference_allreduce(n, size, steps, warmup)
     value = n * bus_bytes(n, size) / t / 1e9
-    cores, model = cpu_info()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
         "n_gpus": n, "steps": steps, "warmup": warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (standard normal)",
-        "config": {"workload": f"all_reduce sum f32, {size // MIB} MiB per rank (bounded sample "
-                               f"of the {args.size_mib} MiB config), world {n}",
+        "same_config": True, "same_steps": steps == args.steps,
+        "config": {"workload": f"all_reduce sum f32, {size // MIB} MiB per rank, world {n} "
+                               f"(BASELINE configs[1] point >= 64 MB)",
                    "op": "all_reduce", "world": n, "bytes_per_rank": size,
-                   "algorithm": "reference default (ring)", "l2": "host path"},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": n, "kind": "reference",
-                         "sample": f"{steps} steps of all_reduce {size // MIB} MiB f32 x {n} "
-                                   f"thread-ranks (one Python process, GIL) on {model}"},
+                   "algorithm": "reference default (ring)", "l2": "host path",
+                   "value_definition": "N * bus_bytes(N, S) / t (as the native arm)"},
+        "cpu_baseline": reference_line_cpu(n, size, t, steps, note),
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -288,7 +309,10 @@ def run_native(args) -> int:
     t = ms * 1e-3
     rt.synchronize()  # surfaces any latched device error
     value = world * bus_bytes(world, size) / t / 1e9
-    per_launch_bytes = bus_bytes(world, size) * args.steps / max(launches, 1)
+    # roofline bytes: NVLink bus bytes (N > 1); HBM read + write of the local
+    # copy (N = 1)
+    roof_bytes = 2.0 * size if world == 1 else bus_bytes(world, size)
+    per_launch_bytes = roof_bytes * args.steps / max(launches, 1)
     t_launch = t * args.steps / max(launches, 1)
     peaks = measured_peaks()
     if world == 1:
@@ -322,17 +346,14 @@ def run_native(args) -> int:
     extra = {}
     if world > 1 and not args.no_secondary:
         extra = secondary(rt, world, rank, dev, size, barrier, max_over_ranks)
-    # ---- CPU baseline (reference package, rank 0, N == 1)
+    # ---- CPU baseline: the reference at the same S and N (thread-ranks),
+    # rank 0, a bounded number of steps
     cpu = None
-    if rank == 0 and world == 1:
+    if rank == 0:
         try:
-            csz = 32 * MIB
-            tc, _ = reference_allreduce(1, csz, 10, 2)
-            cores, model = cpu_info()
-            cpu = {"value": bus_bytes(1, csz) / tc / 1e9, "unit": "GB/s", "cores": 1,
-                   "kind": "reference",
-                   "sample": f"10 steps of all_reduce f32 {csz // MIB} MiB, world 1, reference "
-                             f"mcrdl (baseline/_ref) on {model}"}
+            cs = 3 if world > 2 else 5
+            tc, _ = reference_allreduce(world, size, cs, 1)
+            cpu = reference_line_cpu(world, size, tc, cs)
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
                    "sample": f"failed: {exc!r}"}
@@ -349,10 +370,11 @@ def run_native(args) -> int:
                 "op": "all_reduce", "world": world, "bytes_per_rank": size,
                 "algorithm": tuning.get("winner"),
                 "tuning_table_cell": tuning,
-                "value_definition": ("N * busbw, busbw = 2(N-1)/N*S/t" if world > 1 else
-                                     "2*S/t (local-copy floor: read + write)"),
+                "value_definition": "N * busbw, busbw = bus_bytes(N, S) / t with bus_bytes = "
+                                    "2(N-1)/N*S (N >= 2), S (N = 1, local copy)",
                 "busbw_gbs_per_rank": bus_bytes(world, size) / t / 1e9,
                 "frac_of_900": (bus_bytes(world, size) / t / 1e9 / NVLINK_PEAK) if world > 1 else None,
+                "local_copy_floor_gbs": (2.0 * size / t / 1e9) if world == 1 else None,
                 "l2": f"inputs {args.size_mib} MiB > 126 MB L2 (no flush needed)",
                 "parallelism": f"{world} ranks, one process per GPU",
             },

@@ -127,8 +127,24 @@ mcrdl_status_t mcrdl_comm_caps(const mcrdl_comm* comm, mcrdl_caps_t* caps);
  * destroyed with the comm): which = 0 the host layer's progress lane for async
  * posts (reference: the per-backend lane thread, runtime.py:117-126), 1 / 2 the
  * H2D / D2H staging streams of pipelined host-buffer posts. Never shared
- * between communicators. */
-mcrdl_status_t mcrdl_comm_stream(const mcrdl_comm* comm, int which, void** stream);
+ * between communicators; they stay valid after mcrdl_comm_destroy (until
+ * process exit), since callers may still hold stream-ordered references. */
+mcrdl_status_t mcrdl_comm_stream(mcrdl_comm* comm, int which, void** stream);
+
+/* Tuning table -> MCRDL_ALGO_AUTO (reference: TuningTable.lookup + the
+ * runtime's table load, dispatch.py:135-150, runtime.py:330-332; the paper's
+ * "mix-and-match" reinterpreted as per-op, per-size algorithm choice). For op
+ * kind `kind` (MCRDL_TUNE_ALL_REDUCE / MCRDL_TUNE_BCAST) install n rows
+ * (max_bytes ascending, algo): AUTO takes the first row with message bytes
+ * <= max_bytes, else the last row. n = 0 restores the built-in crossovers.
+ * Every rank must install the same rows (the algorithm is folded into the
+ * flag signature: a disagreement raises ORDER_MISMATCH). */
+enum { MCRDL_TUNE_ALL_REDUCE = 0, MCRDL_TUNE_BCAST = 1, MCRDL_TUNE_KINDS = 2 };
+mcrdl_status_t mcrdl_comm_set_tuning(mcrdl_comm* comm, int kind, int n, const uint64_t* max_bytes,
+                                     const int* algos);
+/* Algorithm (mcrdl_algo_t) the last all_reduce / bcast launch of this
+ * communicator ran (its AUTO resolution), for logs and tests. */
+int mcrdl_comm_last_algo(const mcrdl_comm* comm, int kind);
 /* Latched device error (order mismatch / timeout) of every op issued so far,
  * read without a device sync: call after the stream work completed
  * (WorkHandle.wait / Runtime.synchronize, core.py:312-319, runtime.py:470-494).

@@ -16,12 +16,21 @@ Fixtures:
                           counts {0,1,7,64}, plus f32 all_reduce sums of 1000
                           elements at p=4. Arrays are stored as base64 raw
                           little-endian bytes so floats are exact.
+  cfg5_fusion.json        the reference's FusionManager (middleware.py:241-344)
+                          on the cfg5 step's posting order: the
+                          14 DLRM MLP gradients posted async on a fusion
+                          backend FusionConfig(B = 1 MiB, T = 5 s so grouping
+                          is decided by B alone), p = 2, naive policy. Records
+                          every flush (seq order, member count) and the
+                          posting indices that were not eligible, from the
+                          reference's own CommLog.
   trunc16.json            the reference's Trunc16Codec (middleware.py:43-75):
                           decode(encode(x)) of specials + seeded normals, and
                           live COMPRESSED collectives (CompressionConfig on the
                           inproc backend) for every compressible kind at p=3.
 
     python oracle/make_golden.py trunc16    # only trunc16.json
+    python oracle/make_golden.py cfg5       # only cfg5_fusion.json
 """
 
 from __future__ import annotations
@@ -183,11 +192,57 @@ def trunc16_cases() -> None:
     print("wrote", out, len(records), "compressed cases")
 
 
+CFG5_MLP = [6656, 512, 262144, 512, 65536, 128, 490496, 1024, 1048576, 1024, 1048576, 1024,
+            1024, 1]
+
+
+def cfg5_fusion() -> None:
+    sys.path.insert(0, str(REF_SRC))
+    from mcrdl import AlgorithmPolicy, BackendConfig, Buffer, DType, run_thread_world
+    from mcrdl.middleware import FusionConfig
+
+    def entry(rt, rank):
+        rt.init([BackendConfig("f", transport="inproc", policy=AlgorithmPolicy.naive(),
+                               fusion=FusionConfig(max_bytes=1 << 20, max_wait=5.0))])
+        bufs = [Buffer.from_values(DType.f32, np.full(n, rank + 1, dtype=np.float32))
+                for n in CFG5_MLP]
+        hs = [rt.all_reduce("f", b, async_op=True) for b in bufs]
+        for h in hs:
+            rt.wait(h)
+        rt.synchronize()
+        recs = sorted(rt.comm_log.records(), key=lambda r: r.seq)
+        out = [{"seq": r.seq, "fused": r.fused, "members": r.members, "bytes": r.bytes}
+               for r in recs if r.op == "all_reduce"]
+        ok = all(np.all(b.array == 3.0) for b in bufs)
+        rt.finalize()
+        return out, ok
+
+    res = run_thread_world(2, entry, timeout=60.0)
+    recs, ok = res[0]
+    assert ok and res[1][0] == recs, "reference ranks disagree"
+    fused = [r["members"] for r in recs if r["fused"]]
+    eligible = [i for i, n in enumerate(CFG5_MLP) if 4 * n <= (1 << 20)]
+    doc = {"generator": "oracle/make_golden.py cfg5",
+           "reference": "mcrdl 0.1.0 FusionManager (run_thread_world p=2, inproc, naive)",
+           "posting_order_elems": CFG5_MLP, "dtype": "f32",
+           "fusion": {"max_bytes": 1 << 20, "max_wait_s": 5.0},
+           "eligible_indices": eligible,
+           "flush_members": fused,
+           "unfused_records": sum(1 for r in recs if not r["fused"]),
+           "records": recs}
+    out = OUT / "cfg5_fusion.json"
+    out.write_text(json.dumps(doc, indent=1))
+    print("wrote", out, "flushes", fused)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
-    if sys.argv[1:] == ["trunc16"]:
+    if sys.argv[1:] == ["cfg5"]:
+        cfg5_fusion()
+    elif sys.argv[1:] == ["trunc16"]:
         trunc16_cases()
     else:
         selftest_dumps()
         live_cases()
         trunc16_cases()
+        cfg5_fusion()

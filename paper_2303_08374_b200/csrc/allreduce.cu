@@ -100,16 +100,6 @@ __device__ __forceinline__ void push_packs(const T* in, int64_t n, int64_t g0, i
   for (; i < cnt; i += nt) st16(dst + i * 16, load_pack<T, VEC>(in, g0 + i, n));
 }
 
-__device__ __forceinline__ int64_t seg_len(int64_t npk, int64_t sp, int q, int64_t rb, int64_t re) {
-  // packs of share [rb, re) that exist in segment q
-  const int64_t hi = min(re, npk - int64_t(q) * sp);
-  return hi > rb ? hi - rb : 0;
-}
-__device__ __forceinline__ int nchunks(int64_t len, int64_t chp, int s) {
-  int k = int((len + chp - 1) / chp);
-  return (k == 0 && s == 0) ? 1 : k;  // share 0 always carries a flag (order check)
-}
-
 // TMA bulk-copy streaming (one elected thread): contiguous global -> smem ring
 // (cp.async.bulk + mbarrier) -> global, possibly a peer over NVLink
 // (cp.async.bulk.global.shared::cta). Measured on B200: 16 single-thread CTAs
@@ -1127,6 +1117,9 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
   }
   const int64_t bytes = n * int64_t(sizeof(T));
   const int64_t oneshot_max = half / world / 256 * 256;
+  // AUTO: the installed tuning table first (mcrdl_comm_set_tuning), then the
+  // built-in crossovers
+  if (algo == MCRDL_ALGO_AUTO) algo = tuned_algo(c, MCRDL_TUNE_ALL_REDUCE, uint64_t(bytes));
   if (algo == MCRDL_ALGO_AUTO) {
     // Crossovers measured by the tuner on B200 (profiles/tune_p{2,4}.csv):
     // one-shot pushes (p-1)*S, two-shot 2(p-1)/p*S, so it wins longer at small p.
@@ -1147,6 +1140,8 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
   if (algo == MCRDL_ALGO_NVLS && !(kNvlsType && OP == MCRDL_SUM && c->nvls.ok))
     algo = MCRDL_ALGO_TWO_SHOT;
   if (algo == MCRDL_ALGO_ONE_SHOT && bytes > oneshot_max) algo = MCRDL_ALGO_TWO_SHOT;
+  if (algo == MCRDL_ALGO_DIRECT_WRITE || algo == MCRDL_ALGO_AUTO) algo = MCRDL_ALGO_TWO_SHOT;
+  if (root < 0) c->last_algo[MCRDL_TUNE_ALL_REDUCE] = int(algo);
 
   // Host chunking keeps every launch inside one workspace (or NVLS) half.
   const int64_t room =
@@ -1161,10 +1156,13 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
     const int64_t m = (n - done < chunk_elems) ? (n - done) : chunk_elems;
     mcrdl_status_t st = begin_op(c, stream);
     if (st != MCRDL_OK) return st;
+    // the algorithm is part of the agreement: ranks that resolved AUTO
+    // differently (different tuning rows) raise ORDER_MISMATCH
     const uint32_t sig =
-        root < 0 ? op_sig(kKindAllReduce, dt, OP, sub, uint64_t(m), seq)
-                 : mix32(op_sig(kKindReduce, dt, OP, sub, uint64_t(m), seq), uint64_t(root)) &
-                       ~kSigCodecBit;
+        mix32(root < 0 ? op_sig(kKindAllReduce, dt, OP, sub, uint64_t(m), seq)
+                       : mix32(op_sig(kKindReduce, dt, OP, sub, uint64_t(m), seq), uint64_t(root)),
+              uint64_t(algo)) &
+        ~kSigCodecBit;
     const T* ip = in + done;
     T* op = out + done;
     const int64_t npk = (m + N - 1) / N;
@@ -1183,11 +1181,8 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
       else
         k_ar_oneshot<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, slot, sig);
     } else {
-      const int64_t sp = (npk + world - 1) / world;
-      const int64_t segb = (sp * 16 + 255) / 256 * 256;
       // CTAs per role: one per 32 KiB of segment; 3 roles x gp <= 2 CTAs/SM
       // (MCRDL_AR_GPMAX / MCRDL_AR_CHUNK_KB override, for tuning).
-      int64_t gp = (sp * 16 + (32 << 10) - 1) / (32 << 10);
       static const int64_t gp_env = env_int("MCRDL_AR_GPMAX", 0);
       // Flag chunk: 256 KiB, but 128 KiB for mid-size launches at p >= 4 so a
       // CTA share spans several rows and RS / AG overlap (tools/chunk_ab.sh,
@@ -1197,13 +1192,19 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
       const int64_t chunk_kb =
           chunk_env > 0 ? chunk_env
                         : (world >= 4 && m * int64_t(sizeof(T)) < (int64_t(128) << 20) ? 128 : 256);
-      int64_t gmax = gp_env > 0 ? gp_env : 2 * c->num_sms / 3;
-      if (gmax > kMaxBlocks) gmax = kMaxBlocks;
-      if (gmax < 1) gmax = 1;
-      gp = gp < 1 ? 1 : (gp > gmax ? gmax : gp);
-      const int64_t share = (sp + gp - 1) / gp;
-      int64_t chp = (share + 3999) / 4000;  // <= 4000 chunks per share (12-bit flag step)
-      if (chp < chunk_kb * 64) chp = chunk_kb * 64;  // KiB -> 16-byte packs
+      // RS senders on TMA bulk copies for large launches (aligned buffers):
+      // measured +2-3% at >= 256 MiB, slower below 64 MiB (profiles/tma_ab_r1.log).
+      // MCRDL_AR_TMA=0 disables, =2 forces; MCRDL_AR_TMA_CTAS sets the sender CTAs.
+      static const int64_t tma_on = env_int("MCRDL_AR_TMA", 1);
+      static const int64_t tma_ctas = env_int("MCRDL_AR_TMA_CTAS", 64);
+      const bool big = m * int64_t(sizeof(T)) >= (int64_t(256) << 20);
+      // Share geometry (shares, chunk) comes only from values every rank
+      // agrees on (size, SM budget, env); buffer alignment only picks the
+      // sender flavour (geometry.h two_shot_geo).
+      const bool tma_geo = algo != MCRDL_ALGO_NVLS && (tma_on == 2 || (tma_on == 1 && big));
+      const TwoShotGeo geo =
+          two_shot_geo(npk, world, c->num_sms, chunk_kb, tma_geo, gp_env, tma_ctas, kMaxBlocks);
+      const int64_t sp = geo.sp, segb = geo.segb, gp = geo.gp;
       bool launched = false;
       if constexpr (kNvlsType && OP == MCRDL_SUM) {
         if (algo == MCRDL_ALGO_NVLS) {
@@ -1226,8 +1227,7 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
           const int64_t gpn = std::max<int64_t>(1, std::min<int64_t>(gp, nv_gp));
           const int gcn = int(std::max<int64_t>(1, std::min<int64_t>(nv_gc > 0 ? nv_gc : gpn, gpn)));
           const int ggn = int(std::max<int64_t>(1, std::min<int64_t>(nv_gg > 0 ? nv_gg : gpn, gpn)));
-          int64_t chpn = ((sp + gpn - 1) / gpn + 3999) / 4000;
-          if (chpn < chunk_kb * 64) chpn = chunk_kb * 64;
+          const int64_t chpn = chunk_packs(sp, gpn, chunk_kb);
           const int Gn = int(gcn + gpn + ggn);
           if (vec)
             k_ar_nvls<T, true><<<Gn, kThreads, 0, stream>>>(c->dc, uc, mc, nv_half, ip, op, m, sp,
@@ -1239,29 +1239,9 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
         }
       }
       if (!launched) {
-        // RS senders on TMA bulk copies for large launches (aligned buffers):
-        // measured +2-3% at >= 256 MiB, slower below 64 MiB (profiles/tma_ab_r1.log).
-        // MCRDL_AR_TMA=0 disables, =2 forces; MCRDL_AR_TMA_CTAS sets the sender CTAs.
-        static const int64_t tma_on = env_int("MCRDL_AR_TMA", 1);
-        static const int64_t tma_ctas = env_int("MCRDL_AR_TMA_CTAS", 64);
-        const bool big = m * int64_t(sizeof(T)) >= (int64_t(256) << 20);
         {
-          // Share geometry (shares, chunk) comes only from values every rank
-          // agrees on (size, SM budget, env); buffer alignment only picks the
-          // sender flavour. TMA geometry: few single-thread bulk-copy sender
-          // CTAs leave room for more reducer/gatherer shares.
-          const bool tma_geo = tma_on == 2 || (tma_on == 1 && big);
-          const int gs = int(std::min<int64_t>(gp, tma_ctas));
-          int64_t shares = gp, chs = chp;
-          if (tma_geo) {
-            const int64_t cap = (2 * c->num_sms - gs) / 2;  // gs + 2*gp <= 2 CTAs/SM
-            if (gp_env <= 0 && shares < cap) {
-              shares = std::min<int64_t>(cap, (sp * 16 + (32 << 10) - 1) / (32 << 10));
-              if (shares < 1) shares = 1;
-            }
-            chs = ((sp + shares - 1) / shares + 3999) / 4000;
-            if (chs < chunk_kb * 64) chs = chunk_kb * 64;
-          }
+          const int gs = geo.gs;
+          const int64_t shares = geo.shares, chs = geo.chp;
           // Any geometry disagreement (env knobs) fails as ORDER_MISMATCH
           // instead of folding bytes that have not landed.
           const uint32_t gsig = mix32(mix32(sig, uint64_t(shares)), uint64_t(chs)) & ~kSigCodecBit;

@@ -118,6 +118,12 @@ static const char* cu_str(CUresult r) {
   } while (0)
 
 // ------------------------------------------------------------ bootstrap
+// Setup memsets (pads, symmetric allocations, NVLS flag words) run on the
+// legacy default stream and are waited for on it alone: it does not wait for
+// non-blocking streams, so a co-located peer rank's spinning kernel never
+// stalls a setup, and no stream is created per communicator.
+static const cudaStream_t kSetupStream = nullptr;
+
 static mcrdl_status_t host_allgather(mcrdl_comm* c, const void* send, void* recv, size_t n) {
   if (c->world == 1) {
     memcpy(recv, send, n);
@@ -491,9 +497,9 @@ static mcrdl_status_t setup_nvls(mcrdl_comm* c, uint64_t bytes) {
     for (int h = 0; h < 2; ++h)
       if (cudaMemsetAsync(reinterpret_cast<uint8_t*>(nv.uc_ptr) + (h + 1) * (bytes / 2) -
                               kNvlsFlagBytes,
-                          0, kNvlsFlagBytes, c->aux) != cudaSuccess)
+                          0, kNvlsFlagBytes, kSetupStream) != cudaSuccess)
         ok = 0;
-    if (cudaStreamSynchronize(c->aux) != cudaSuccess) ok = 0;
+    if (cudaStreamSynchronize(kSetupStream) != cudaSuccess) ok = 0;
   }
   if ((st = host_allgather(c, &ok, oks, sizeof(int))) != MCRDL_OK) return st;
   for (int r = 0; r < c->world; ++r) ok &= oks[r];
@@ -609,8 +615,6 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
     mcrdl_comm_destroy(c);
     return s;
   };
-  MCRDL_CUDA_CHECK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
-  for (auto& x : c->xfer) MCRDL_CUDA_CHECK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
 
   // Job id from rank 0 (fresh random per init) names the sockets; the device
   // UUIDs tell which ranks share a GPU.
@@ -640,10 +644,14 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
     c->ranks_per_device = std::max(c->ranks_per_device, same);
     budget = std::min<int>(budget, all[q].sms);
   }
-  // Co-located ranks: every rank's grids (at most 2 CTAs per budgeted SM, up
-  // to two chains in flight per rank) must be resident at once, or a spinning
-  // grid would wait for a peer grid that cannot be scheduled.
-  if (c->ranks_per_device > 1) budget = std::min(budget, dev_sms / (2 * c->ranks_per_device));
+  // Co-located ranks: every rank's grids must be resident at once, or a
+  // spinning grid would wait for a peer grid that cannot be scheduled. Grids
+  // are sized at up to 2 CTAs (512 threads, <= 64 regs) per budgeted SM, up
+  // to two chains (send + recv, or a collective and a recv) are in flight per
+  // rank, and transient kernels of the host framework share the SMs: a
+  // quarter of the device per rank-share (measured: p = 4 send/recv rings
+  // stall with 18 SMs per rank, pass with 8).
+  if (c->ranks_per_device > 1) budget = std::min(budget, dev_sms / (4 * c->ranks_per_device));
   c->num_sms = std::max(1, budget);
   if (c->ranks_per_device > 1) {
     // Lazy kernel loading waits for the context to idle: a co-located rank's
@@ -689,8 +697,8 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   // Setup memsets run on the comm's private stream and are waited for on
   // that stream only: a device-wide sync could wait on spinning kernels of
   // co-located ranks whose peers have not launched yet.
-  MCRDL_CUDA_CHECK(cudaMemsetAsync(reinterpret_cast<void*>(c->base.ptr[rank]), 0, kPadBytes, c->aux));
-  MCRDL_CUDA_CHECK(cudaStreamSynchronize(c->aux));
+  MCRDL_CUDA_CHECK(cudaMemsetAsync(reinterpret_cast<void*>(c->base.ptr[rank]), 0, kPadBytes, kSetupStream));
+  MCRDL_CUDA_CHECK(cudaStreamSynchronize(kSetupStream));
 
   // NVLS buffer: half the workspace size by default; MCRDL_NVLS_BYTES=0 disables.
   uint64_t nvls_bytes = workspace_bytes / 2;
@@ -754,9 +762,10 @@ mcrdl_status_t mcrdl_comm_destroy(mcrdl_comm* c) {
     if (ch.ev) cudaEventDestroy(ch.ev);
   if (c->trace_host) cudaFreeHost(c->trace_host);
   if (c->oplog_host) cudaFreeHost(c->oplog_host);
-  if (c->aux) cudaStreamDestroy(c->aux);
-  for (auto& x : c->xfer)
-    if (x) cudaStreamDestroy(x);
+  // The comm's streams are NOT destroyed: host frameworks keep stream-ordered
+  // references (e.g. torch's caching allocator records events on a lane
+  // stream when a tensor used there is freed, possibly after finalize). A
+  // handful of streams per communicator live until process exit.
   for (auto& kv : c->fd_stash) close(kv.second);
   if (c->listen_fd >= 0) close(c->listen_fd);
   delete c;
@@ -803,11 +812,41 @@ mcrdl_status_t mcrdl_comm_caps(const mcrdl_comm* c, mcrdl_caps_t* caps) {
   return MCRDL_OK;
 }
 
-mcrdl_status_t mcrdl_comm_stream(const mcrdl_comm* c, int which, void** stream) {
+mcrdl_status_t mcrdl_comm_stream(mcrdl_comm* c, int which, void** stream) {
   if (c == nullptr || stream == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL argument");
   if (which < 0 || which > 2) return set_error(MCRDL_ERR_VALIDATION, "stream index %d", which);
-  *stream = reinterpret_cast<void*>(which == 0 ? c->aux : c->xfer[which - 1]);
+  // created on first request: a communicator that never posts async work
+  // adds no stream (co-located ranks share the device's hardware queues)
+  cudaStream_t& s = which == 0 ? c->aux : c->xfer[which - 1];
+  if (s == nullptr) {
+    MCRDL_CUDA_CHECK(cudaSetDevice(c->device));
+    MCRDL_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  }
+  *stream = reinterpret_cast<void*>(s);
   return MCRDL_OK;
+}
+
+mcrdl_status_t mcrdl_comm_set_tuning(mcrdl_comm* c, int kind, int n, const uint64_t* max_bytes,
+                                     const int* algos) {
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  if (kind < 0 || kind >= MCRDL_TUNE_KINDS) return set_error(MCRDL_ERR_VALIDATION, "tuning kind %d", kind);
+  if (n < 0 || n > 64 || (n > 0 && (max_bytes == nullptr || algos == nullptr)))
+    return set_error(MCRDL_ERR_VALIDATION, "tuning rows: n = %d", n);
+  std::vector<std::pair<uint64_t, int>> rows;
+  for (int i = 0; i < n; ++i) {
+    if (algos[i] < MCRDL_ALGO_AUTO || algos[i] > MCRDL_ALGO_DIRECT_WRITE)
+      return set_error(MCRDL_ERR_VALIDATION, "tuning row %d: algorithm %d", i, algos[i]);
+    if (i > 0 && max_bytes[i] <= max_bytes[i - 1])
+      return set_error(MCRDL_ERR_VALIDATION, "tuning rows: max_bytes must strictly increase");
+    rows.emplace_back(max_bytes[i], algos[i]);
+  }
+  c->tune[kind] = std::move(rows);
+  return MCRDL_OK;
+}
+
+int mcrdl_comm_last_algo(const mcrdl_comm* c, int kind) {
+  if (c == nullptr || kind < 0 || kind >= MCRDL_TUNE_KINDS) return -1;
+  return c->last_algo[kind];
 }
 
 mcrdl_status_t mcrdl_comm_status(mcrdl_comm* c) {
@@ -842,12 +881,12 @@ mcrdl_status_t mcrdl_symm_alloc(mcrdl_comm* c, uint64_t bytes, void** local_ptr)
     unmap_region(c, rg);
     return st;
   }
-  MCRDL_CUDA_CHECK(cudaMemsetAsync(reinterpret_cast<void*>(rg.ptr[c->rank]), 0, rg.bytes, c->aux));
+  MCRDL_CUDA_CHECK(cudaMemsetAsync(reinterpret_cast<void*>(rg.ptr[c->rank]), 0, rg.bytes, kSetupStream));
   if (c->nvls.ok && mg > 0 && (st = bind_multicast(c, &rg)) != MCRDL_OK) {
     unmap_region(c, rg);
     return st;
   }
-  MCRDL_CUDA_CHECK(cudaStreamSynchronize(c->aux));
+  MCRDL_CUDA_CHECK(cudaStreamSynchronize(kSetupStream));
   c->symm.push_back(rg);
   *local_ptr = reinterpret_cast<void*>(rg.ptr[c->rank]);
   return MCRDL_OK;

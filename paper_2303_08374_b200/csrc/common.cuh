@@ -23,6 +23,7 @@
 #include <stdio.h>
 
 #include "../../include/mcrdl_nvl.h"
+#include "geometry.h"
 
 namespace mcrdl {
 
@@ -475,12 +476,5 @@ __device__ __forceinline__ void block_copy(uint8_t* dst, const uint8_t* src, int
   for (int64_t i = done + tid; i < n; i += nt) dst[i] = src[i];
 }
 
-// [s, e) share of `len` bytes for block b of G (16-byte aligned starts).
-__device__ __forceinline__ void byte_share(int64_t len, int b, int G, int64_t& s, int64_t& e) {
-  int64_t chunk = (len + G - 1) / G;
-  chunk = (chunk + 15) & ~int64_t(15);
-  s = min(len, int64_t(b) * chunk);
-  e = min(len, s + chunk);
-}
 
 }  // namespace mcrdl

@@ -54,11 +54,6 @@ constexpr int64_t kPairCtaBytes = 32 << 10;   // one CTA per 32 KiB of a pair
 // 418 us at 256 KiB, 64 KiB equal to 128 KiB, <= 16 MiB neutral;
 // profiles/xgeo_ab_r1_p4.log).
 constexpr int64_t kChunkBytes = 128 << 10;
-constexpr int64_t kMaxSteps = 4000;           // < 4096 (12-bit flag step)
-
-__device__ __host__ __forceinline__ int64_t rounds_for(int64_t bytes, int64_t slot) {
-  return bytes <= slot ? 1 : (bytes + slot - 1) / slot;
-}
 __device__ __forceinline__ uint32_t pair_sig(uint32_t base, int64_t bytes) {
   // user (not wire) bytes, codec bit carried through from the base
   return (mix32(base, uint64_t(bytes)) & 0x7FFFFu) | (base & kSigCodecBit);
@@ -120,48 +115,6 @@ __device__ __forceinline__ void block_decode16(uint8_t* dst, const uint8_t* src,
   uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
   for (int64_t e = done + tid; e < ne; e += nt) d32[e] = uint32_t(__ldcg(s16 + e)) << 16;
 }
-// CTAs serving one pair: a function of the pair's byte count only.
-__device__ __host__ __forceinline__ int pair_ctas(int64_t bytes, int gmax, int64_t per_cta,
-                                                  int64_t wide_min) {
-  if (wide_min > 0 && bytes >= wide_min) per_cta *= 4;
-  int64_t g = (bytes + per_cta - 1) / per_cta;
-  return int(g < 1 ? 1 : (g > gmax ? gmax : g));
-}
-__device__ __forceinline__ int64_t pair_chunk(int64_t bytes, int g, int64_t chunk_min) {
-  // (~4 smaller chunks per share for push / copy-out overlap measured WORSE
-  // for mid-size pairs: p = 4 all_to_allv 16 MiB 275 vs 325 GB/s — the extra
-  // flag round trips cost more than the overlap gains)
-  int64_t per = (bytes + g - 1) / g;
-  int64_t ch = (per + kMaxSteps - 1) / kMaxSteps;
-  ch = (ch + 15) & ~int64_t(15);
-  return ch > chunk_min ? ch : chunk_min;
-}
-
-// Share s of round t of a pair moving B bytes: [a, e) relative to the round,
-// in n chunks of `ch` bytes. A 0-byte pair still carries one empty chunk on
-// share 0 (its flag is the order check / barrier).
-struct Span {
-  int64_t a, e;
-  int n;
-};
-__device__ __forceinline__ Span span_of(int64_t B, int64_t slot, int g, int64_t ch, int64_t t, int s) {
-  Span sp{0, 0, 0};
-  if (s >= g || t >= rounds_for(B, slot)) return sp;
-  const int64_t len = min(slot, B - t * slot);
-  // Share boundaries come from round 0 (the longest) in EVERY round: CTA s
-  // owns the same slot bytes each round, so the receiver's per-share ack of
-  // round t frees exactly what sender CTA s overwrites in round t+1 (a
-  // shorter last round must not shift shares onto bytes another receiver
-  // CTA is still landing).
-  int64_t chunk = (min(slot, B) + g - 1) / g;
-  chunk = (chunk + 15) & ~int64_t(15);
-  sp.a = min(len, int64_t(s) * chunk);
-  sp.e = min(len, sp.a + chunk);
-  sp.n = int((sp.e - sp.a + ch - 1) / ch);
-  if (B == 0 && s == 0 && t == 0) sp.n = 1;
-  return sp;
-}
-
 // Per-peer geometry of this CTA's role, computed once by thread `peer`:
 // 64-bit divisions are ~70-instruction subroutines, and every thread of
 // every row recomputing them cost ~8 us of latency per op.
@@ -398,8 +351,24 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   }
   mcrdl_status_t st = begin_op(c, stream);
   if (st != MCRDL_OK) return st;
+  // Geometry knobs (tools/xgeo_ab.sh); every rank must see the same values.
+  static const int64_t pair_kb = env_int("MCRDL_X_PAIR_KB", kPairCtaBytes >> 10);
+  static const int64_t chunk_kb = env_int("MCRDL_X_CHUNK_KB", kChunkBytes >> 10);
+  // Pairs >= 8 MiB: 128 KiB of pair per CTA (fewer, longer shares). p = 4
+  // 32/64 MiB all_to_allv +11/+8 %, p = 2 16/32 MiB +17/+13 %, other sizes
+  // neutral; a 4 MiB threshold costs p = 4 16 MiB (profiles/xwide_ab_r1_p2p4.log).
+  static const int64_t wide_mb = env_int("MCRDL_X_WIDE_MB", 8);
+  const int64_t pair_cta = (pair_kb > 0 ? pair_kb : kPairCtaBytes >> 10) << 10;
+  const int64_t chunk_min = (chunk_kb > 0 ? chunk_kb : kChunkBytes >> 10) << 10;
+  const int64_t wide_min = wide_mb > 0 ? wide_mb << 20 : 0;
+  // The knobs are part of the pair agreement: ranks with different MCRDL_X_*
+  // values raise ORDER_MISMATCH instead of landing half-written shares.
+  ExchangeSpec spg = sp;
+  spg.sig_base =
+      mix32(mix32(mix32(sp.sig_base, uint64_t(pair_cta)), uint64_t(chunk_min)), uint64_t(wide_min)) &
+      ~kSigCodecBit;
   const int64_t ll_max = sp.codec ? -1 : exchange_ll_max();
-  if (ll_max >= 0 && try_exchange_ll(c, sp, ll_max, stream, &st)) return st;
+  if (ll_max >= 0 && try_exchange_ll(c, spg, ll_max, stream, &st)) return st;
   XArgs a;
   memset(&a, 0, sizeof(a));
   for (int r = 0; r < c->world; ++r) {
@@ -416,17 +385,10 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   a.esize = sp.esize;
   a.codec = sp.codec;
   a.ll_max = ll_max;
-  // Geometry knobs (tools/xgeo_ab.sh); every rank must see the same values.
-  static const int64_t pair_kb = env_int("MCRDL_X_PAIR_KB", kPairCtaBytes >> 10);
-  static const int64_t chunk_kb = env_int("MCRDL_X_CHUNK_KB", kChunkBytes >> 10);
-  a.pair_cta = (pair_kb > 0 ? pair_kb : kPairCtaBytes >> 10) << 10;
-  a.chunk_min = (chunk_kb > 0 ? chunk_kb : kChunkBytes >> 10) << 10;
-  // Pairs >= 8 MiB: 128 KiB of pair per CTA (fewer, longer shares). p = 4
-  // 32/64 MiB all_to_allv +11/+8 %, p = 2 16/32 MiB +17/+13 %, other sizes
-  // neutral; a 4 MiB threshold costs p = 4 16 MiB (profiles/xwide_ab_r1_p2p4.log).
-  static const int64_t wide_mb = env_int("MCRDL_X_WIDE_MB", 8);
-  a.wide_min = wide_mb > 0 ? wide_mb << 20 : 0;
-  a.sig_base = (sp.sig_base & ~kSigCodecBit) | (sp.codec ? kSigCodecBit : 0u);
+  a.pair_cta = pair_cta;
+  a.chunk_min = chunk_min;
+  a.wide_min = wide_min;
+  a.sig_base = spg.sig_base | (sp.codec ? kSigCodecBit : 0u);
   a.slot = c->dc.half_bytes / c->world / 256 * 256;
   a.gmax = c->num_sms < kMaxBlocks ? c->num_sms : kMaxBlocks;  // 2 roles -> 2 CTAs/SM
   if (a.gmax < 1) a.gmax = 1;

@@ -179,9 +179,16 @@ mcrdl_status_t mcrdl_all_gatherv(mcrdl_comm* c, const void* in, void* out, const
         ro[q] = displs[c->rank] * es;
         b[q] = rcounts[c->rank] * es;
       }
+      // Direct writes place rank q's block at ITS displs[q] in every output:
+      // every rank must pass the same rcounts and displs (fold them into the
+      // signature so a disagreement raises ORDER_MISMATCH instead of
+      // scattering blocks to the wrong place).
+      uint32_t sig = op_sig(kKindAllGatherv, dtype, 1, -1, 0, seq);
+      for (int r = 0; r < c->world; ++r)
+        sig = mix32(mix32(sig, uint64_t(rcounts[r])), uint64_t(displs[r]));
+      sig &= ~kSigCodecBit;
       mcrdl_status_t st;
-      if (try_exchange_symm(c, in, out, uint64_t(end), so, ro, b, mx,
-                            op_sig(kKindAllGatherv, dtype, 1, -1, 0, seq),
+      if (try_exchange_symm(c, in, out, uint64_t(end), so, ro, b, mx, sig,
                             reinterpret_cast<cudaStream_t>(stream), &st))
         return st;
     }
@@ -245,11 +252,15 @@ mcrdl_status_t mcrdl_bcast(mcrdl_comm* c, void* buf, uint64_t count, mcrdl_dtype
   // profiles/bcast_r1_p4.csv). The choice uses only values every rank agrees
   // on (the kernel copes with unaligned buffers and partial packs).
   const bool nv_ok = c->nvls.ok && nb > 0 && !codec;  // the multicast path moves raw bytes
+  if (algo == MCRDL_ALGO_AUTO) algo = tuned_algo(c, MCRDL_TUNE_BCAST, uint64_t(nb));
   if (nv_ok && (algo == MCRDL_ALGO_NVLS ||
                 (algo == MCRDL_ALGO_AUTO && c->world >= 3 &&
-                 nb >= (int64_t(32) << 20) / (c->world - 1))))
+                 nb >= (int64_t(32) << 20) / (c->world - 1)))) {
+    c->last_algo[MCRDL_TUNE_BCAST] = MCRDL_ALGO_NVLS;
     return launch_bcast_nvls(c, reinterpret_cast<uint8_t*>(buf), nb, root, int(dtype), count, seq,
                              reinterpret_cast<cudaStream_t>(stream));
+  }
+  c->last_algo[MCRDL_TUNE_BCAST] = MCRDL_ALGO_DIRECT_WRITE;
   ExchangeSpec s = empty_spec(es, op_sig(kKindBcast, dtype, 0, root, count, seq));
   s.codec = codec;
   if (c->rank == root) {

@@ -57,9 +57,9 @@ struct mcrdl_comm {
   // every rank (min) because launch geometry must match across ranks.
   int num_sms = 0;
   int ranks_per_device = 1;  // max ranks sharing one physical GPU in this comm
-  // The comm's own non-blocking stream: setup memsets, and the host layer's
-  // lane for async posts (mcrdl_comm_stream). One per comm, never pooled, so
-  // two communicators (e.g. co-located ranks) never share a stream.
+  // The comm's own non-blocking stream, created on first request: the host
+  // layer's lane for async posts (mcrdl_comm_stream). One per comm, never
+  // pooled, so two communicators (e.g. co-located ranks) never share one.
   cudaStream_t aux = nullptr;
   cudaStream_t xfer[2] = {nullptr, nullptr};  // H2D / D2H staging (pipelined host posts)
   int fd_tag = 0;                              // fd-exchange round counter
@@ -92,6 +92,9 @@ struct mcrdl_comm {
   uint64_t* trace_host = nullptr;  // trace builds: kMaxBlocks x kTraceSlots stamps
   uint64_t* oplog_host = nullptr;  // kOpLogSlots x {tag0, t0, tag1, t1} (mapped)
   uint64_t log_seq = 0;            // last log id handed to a launch
+  // tuning rows per MCRDL_TUNE_* kind: (max_bytes ascending, algorithm)
+  std::vector<std::pair<uint64_t, int>> tune[MCRDL_TUNE_KINDS];
+  int last_algo[MCRDL_TUNE_KINDS] = {0, 0};
 };
 
 namespace mcrdl {
@@ -117,6 +120,15 @@ enum : int { kChainCollective = 0, kChainSend = 1, kChainRecv = 2 };
 // *off = p - region base. Every rank maps every rank's copy at ptr[r].
 const Region* find_symm(const mcrdl_comm* c, const void* p, uint64_t bytes, uint64_t* off);
 mcrdl_status_t begin_op(mcrdl_comm* comm, cudaStream_t stream, int chain = kChainCollective);
+
+// Tuning-table algorithm for `bytes` of op `kind`, or AUTO if no rows.
+inline mcrdl_algo_t tuned_algo(const mcrdl_comm* c, int kind, uint64_t bytes) {
+  const auto& rows = c->tune[kind];
+  if (rows.empty()) return MCRDL_ALGO_AUTO;
+  for (const auto& r : rows)
+    if (bytes <= r.first) return mcrdl_algo_t(r.second);
+  return mcrdl_algo_t(rows.back().second);
+}
 
 inline int64_t env_int(const char* name, int64_t dflt) {
   const char* e = getenv(name);

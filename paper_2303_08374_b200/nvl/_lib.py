@@ -39,6 +39,8 @@ SIGNATURES = {
     "mcrdl_comm_caps": (c_int, [_P, POINTER(Caps)]),
     "mcrdl_comm_status": (c_int, [_P]),
     "mcrdl_comm_stream": (c_int, [_P, c_int, POINTER(c_void_p)]),
+    "mcrdl_comm_set_tuning": (c_int, [_P, c_int, c_int, POINTER(c_uint64), POINTER(c_int)]),
+    "mcrdl_comm_last_algo": (c_int, [_P, c_int]),
     "mcrdl_comm_log_id": (c_uint64, [_P]),
     "mcrdl_comm_op_time": (c_int, [_P, c_uint64, c_uint64, _I64P]),
     "mcrdl_symm_alloc": (c_int, [_P, c_uint64, POINTER(c_void_p)]),

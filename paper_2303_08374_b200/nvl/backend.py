@@ -263,7 +263,42 @@ class NvlBackendInstance:
                             runtime.timeout)
         # Lane = the communicator's own stream (not one from torch's
         # round-robin pool, which hands the same stream to several callers).
-        self.stream = self.comm.stream(0)
+        self._lane = None  # created on first async post (see the stream property)
+        self.tuning_rows = {}
+        self.install_tuning(runtime.algorithm_table)
+
+    @property
+    def stream(self):
+        """The progress lane (reference: the backend's lane thread,
+        runtime.py:117-126): Runtime.lane_stream when the host set one (one
+        lane for all of a rank's backends, e.g. co-located ranks), else the
+        communicator's own stream, created on first use."""
+        if self._lane is None:
+            self._lane = self.runtime.lane_stream or self.comm.stream(0)
+        return self._lane
+
+    # ------------------------------------------------------------ tuning
+    TUNE_KINDS = {CommOpKind.all_reduce: 0, CommOpKind.bcast: 1}  # MCRDL_TUNE_*
+
+    def install_tuning(self, table) -> None:
+        """Push the table's per-size algorithm rows for this world into the
+        communicator: AUTO then resolves in the C layer (mcrdl_comm_set_tuning).
+        No table / no cell: the library's built-in crossovers. Every rank
+        loads the same table, so every rank resolves AUTO alike."""
+        from ..dispatch import algorithm_rows
+
+        lib, c = self.comm.lib, self.comm.handle
+        for kind, code in self.TUNE_KINDS.items():
+            rows = algorithm_rows(table, kind, self.world_size, self.name)
+            self.tuning_rows[kind] = rows
+            mb = (ctypes.c_uint64 * max(len(rows), 1))(*[r[0] for r in rows])
+            al = (ctypes.c_int * max(len(rows), 1))(*[ALGO_CODES[canonical(kind, r[1])] for r in rows])
+            _lib.check(lib.mcrdl_comm_set_tuning(c, code, len(rows), mb, al))
+
+    def last_algorithm(self, kind: CommOpKind) -> Optional[str]:
+        """Algorithm the last AUTO-resolved launch of `kind` ran (C layer)."""
+        code = self.comm.lib.mcrdl_comm_last_algo(self.comm.handle, self.TUNE_KINDS[kind])
+        return _ALGO_NAMES.get(code)
 
     # ------------------------------------------------------------ properties
     @property
@@ -565,10 +600,13 @@ class NvlBackendInstance:
             # Ops of one communicator execute in issue order (the C layer
             # chains streams), so an event after the last op covers them all.
             last = self._last_raw
-            if last is not None and last != int(self.stream.cuda_stream):
+            if self._lane is None:  # no async work yet: the last inline op's stream
+                ev.record(torch.cuda.ExternalStream(last, device=self.device) if last is not None
+                          else torch.cuda.current_stream(self.device))
+            elif last is not None and last != int(self._lane.cuda_stream):
                 ev.record(torch.cuda.ExternalStream(last, device=self.device))
             else:
-                ev.record(self.stream)
+                ev.record(self._lane)
             pending = list(self._pending)
         ce = CompletionEvent(self.name, cuda_event=ev)
         ce._pending = pending  # type: ignore[attr-defined]
@@ -642,6 +680,8 @@ class NvlBackendInstance:
                 o = st.dev(req.output, upload=req.output is req.input, download=True)
                 chk(lib.mcrdl_all_reduce(c, _ptr(i), _ptr(o), req.input.count, dt.code, op, algo,
                                          seq, s))
+                if algo & 0xFF == 0 and p > 1:  # AUTO: log what the C layer resolved
+                    req._algorithm = self.last_algorithm(kind)
             elif kind is CommOpKind.reduce:
                 o = (st.dev(req.output, upload=req.output is req.input, download=True)
                      if rank == req.root else None)
@@ -682,6 +722,8 @@ class NvlBackendInstance:
             b = st.dev(req.output, upload=True, download=True)
             chk(lib.mcrdl_bcast(c, _ptr(b), req.output.count, req.output.dtype.code, req.root,
                                 algo, seq, s))
+            if algo & 0xFF == 0 and p > 1:
+                req._algorithm = self.last_algorithm(kind)
             return
 
         if kind in (CommOpKind.all_gather, CommOpKind.all_gatherv):

@@ -113,9 +113,19 @@ class Runtime:
         # collective's native launch (co-located thread-rank tests launch each
         # op's kernels together; tests/gpu_worker.py). None in production.
         self.launch_hook = None
+        # Optional torch stream used as the progress lane by every nvlink
+        # backend of this runtime (None: one communicator-owned stream each).
+        self.lane_stream = None
         path = os.environ.get(ENV_TUNING_TABLE)
         if path:
             self.tuning_table = dispatch.load_table(path)
+        # Algorithm table behind AUTO on nvlink backends (per op, per size):
+        # MCRDL_TUNING_TABLE when set (runtime.py:330-332), else the measured
+        # table shipped with the package; MCRDL_ALGO_TABLE=off keeps the
+        # library's built-in crossovers.
+        self.algorithm_table: Optional[dispatch.TuningTable] = None
+        if os.environ.get("MCRDL_ALGO_TABLE", "") not in ("off", "0"):
+            self.algorithm_table = self.tuning_table or dispatch.default_algorithm_table()
 
     # -------------------------------------------------------------- lifecycle
     def init(self, backends: Sequence[Union[BackendConfig, str]]) -> None:

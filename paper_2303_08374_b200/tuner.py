@@ -91,7 +91,12 @@ def statistic_value(durations: Sequence[float], statistic: str) -> float:
     raise ValidationError("statistic", f"one of {STATISTICS}")
 
 
-_SYMM_CACHE: dict = {}
+_SYMM_CACHE: dict = {}  # keyed by the owning communicator: freed with it
+
+
+def _comm_key(rt, backend: str):
+    comm = rt._instance(backend).comm
+    return (id(comm), int(comm.handle.value or 0))
 
 
 def make_op(rt, backend: str, kind: CommOpKind, nbytes: int, dtype: DType,
@@ -111,7 +116,7 @@ def make_op(rt, backend: str, kind: CommOpKind, nbytes: int, dtype: DType,
         return torch.ones(count, dtype=td, device=dev)
 
     if symmetric and kind is CommOpKind.all_reduce:
-        key = (backend, n, dtype)
+        key = (_comm_key(rt, backend), n, dtype)
         if key not in _SYMM_CACHE:
             pair = [rt.symmetric_empty(backend, n, dtype) for _ in range(2)]
             for x in pair:
@@ -136,7 +141,7 @@ def make_op(rt, backend: str, kind: CommOpKind, nbytes: int, dtype: DType,
     def out_t(count):  # symmetric output (zero-copy exchange) when asked
         if not symmetric:
             return t(count)
-        key = (backend, "out", count, dtype)
+        key = (_comm_key(rt, backend), "out", count, dtype)
         if key not in _SYMM_CACHE:
             _SYMM_CACHE[key] = rt.symmetric_empty(backend, count, dtype)
         return _SYMM_CACHE[key]

@@ -125,5 +125,7 @@ if __name__ == "__main__":
               f"launches={rep.get('launches')} failures={len(rep['failures'])}")
         for f in rep["failures"][:20]:
             print("   ", f)
+        for x in rep.get("log_tail", []):
+            print("     log", x)
         bad += len(rep["failures"]) + (rep["exit"] != 0)
     sys.exit(1 if bad else 0)

@@ -59,7 +59,7 @@ class _Memo:
     """Co-located ranks generate the same seeded inputs: share them (bounded
     LRU of read-only arrays, so no rank can mutate another rank's view)."""
 
-    def __init__(self, max_bytes: int = 3 << 30):
+    def __init__(self, max_bytes: int = 6 << 30):
         self.max_bytes = max_bytes
         self.items: "OrderedDict" = OrderedDict()
         self.bytes = 0
@@ -127,6 +127,17 @@ def from_dev(t: torch.Tensor, dtype: DType) -> np.ndarray:
     if dtype is DType.bf16:
         return t.view(torch.int16).numpy().view(np.uint16)
     return t.numpy()
+
+
+def _raw_stream(device: int):
+    """A non-blocking stream created directly with the driver (not from
+    torch's round-robin pool, which hands one stream to several callers)."""
+    from cuda.bindings import driver as drv
+
+    err, s = drv.cuStreamCreate(drv.CUstream_flags.CU_STREAM_NON_BLOCKING)
+    if err != drv.CUresult.CUDA_SUCCESS:
+        raise RuntimeError(f"cuStreamCreate: {err}")
+    return torch.cuda.ExternalStream(int(s), device=device)
 
 
 class Shared:
@@ -689,38 +700,79 @@ def sc_p2p(cx: Ctx):
     message larger than the 32 MiB mailbox (recv posted first, async), the
     tuner's rank 0<->1 ping-pong (tuner.py:128-145), self-send, staged numpy
     buffers, CUDA-graph replay, and LengthMismatch (runtime.py:256-260) on a
-    dedicated backend."""
+    dedicated backend.
+
+    send/recv do not go through the collective launch rendezvous, so for
+    co-located ranks every step allocates its buffers first and then meets
+    the peers (cx.lockstep) before launching: no rank is inside a
+    device-synchronizing allocation while a peer's kernel waits on it."""
     p, r, dev = cx.p, cx.r, cx.dev
     nxt, prv = (r + 1) % p, (r - 1) % p
-    for n in (0, 1, 1000, 131072, 131073, 3_000_001):
+    only = os.environ.get("MCRDL_P2P_PARTS")  # debugging: run a subset of the parts
+    parts = set(only.split(",")) if only else {"ring", "queued", "rendezvous", "pingpong", "self",
+                                                "host", "graph", "lenm"}
+    for n in ((0, 1, 1000, 131072, 131073, 3_000_001) if "ring" in parts else ()):
         x = [values(DType.f32, n, "p2p", n, q) for q in range(p)]
         dst = torch.full((n,), -1.0, device=dev)
-        cx.rt.send(cx.b, Buffer(to_dev(x[r], DType.f32, dev)), nxt)
+        src = to_dev(x[r], DType.f32, dev)
+        cx.lockstep(("ring", n))
+        cx.rt.send(cx.b, Buffer(src), nxt)
         cx.rt.recv(cx.b, Buffer(dst), prv)
         cx.check(f"p2p/ring/{n}", from_dev(dst, DType.f32), x[prv])
     # 40 sends queued before their receives (eager: headers and slots free)
+    if "queued" in parts:
+        _p2p_queued(cx, nxt, prv)
+    if "rendezvous" in parts:
+        _p2p_rendezvous(cx, nxt, prv)
+    if "pingpong" in parts:
+        _p2p_pingpong(cx)
+    if "self" in parts:
+        _p2p_self(cx)
+    if "host" in parts:
+        _p2p_host(cx, nxt, prv)
+    if "graph" in parts:
+        _p2p_graph(cx, nxt, prv)
+    if "lenm" in parts:
+        _p2p_lenm(cx)
+
+
+def _p2p_queued(cx, nxt, prv):
+    p, r, dev = cx.p, cx.r, cx.dev
     xs = [[values(DType.i64, 100 + k, "p2pq", k, q) for q in range(p)] for k in range(40)]
-    for k in range(40):
-        cx.rt.send(cx.b, Buffer(to_dev(xs[k][r], DType.i64, dev)), nxt)
+    srcs = [to_dev(xs[k][r], DType.i64, dev) for k in range(40)]
     outs = [torch.zeros(100 + k, dtype=torch.int64, device=dev) for k in range(40)]
+    cx.lockstep(("queued",))
+    for k in range(40):
+        cx.rt.send(cx.b, Buffer(srcs[k]), nxt)
     for k in range(40):
         cx.rt.recv(cx.b, Buffer(outs[k]), prv)
     for k in range(40):
         cx.check(f"p2p/queued/{k}", from_dev(outs[k], DType.i64), xs[k][prv])
-    # rendezvous: 40 MiB + 12 B > mailbox; the recv runs on the lane stream
+
+
+def _p2p_rendezvous(cx, nxt, prv):
+    """40 MiB + 12 B > mailbox; the recv runs on the lane stream."""
+    p, r, dev = cx.p, cx.r, cx.dev
     n = (10 << 20) + 3
     x = [values(DType.f32, n, "p2pbig", q) for q in range(p)]
     dst = torch.zeros(n, device=dev)
+    src = to_dev(x[r], DType.f32, dev)
+    cx.lockstep(("rendezvous",))
     h = cx.rt.recv(cx.b, Buffer(dst), prv, async_op=True)
-    cx.rt.send(cx.b, Buffer(to_dev(x[r], DType.f32, dev)), nxt)
+    cx.rt.send(cx.b, Buffer(src), nxt)
     h.wait()
     torch.cuda.current_stream().wait_stream(cx.rt._instance(cx.b).stream)
     cx.check("p2p/rendezvous", from_dev(dst, DType.f32), x[prv])
-    # ping-pong between ranks 0 and 1, bf16 payload
+
+
+def _p2p_pingpong(cx):
+    """Ping-pong between ranks 0 and 1, bf16 payload."""
+    p, r, dev = cx.p, cx.r, cx.dev
+    y = [values(DType.bf16, 70000, "pp", q) for q in range(2)]
+    mine = to_dev(y[min(r, 1)], DType.bf16, dev)
+    got = torch.zeros_like(mine)
+    cx.lockstep(("pingpong",))
     if p >= 2 and r < 2:
-        y = [values(DType.bf16, 70000, "pp", q) for q in range(2)]
-        mine = to_dev(y[r], DType.bf16, dev)
-        got = torch.zeros_like(mine)
         if r == 0:
             cx.rt.send(cx.b, Buffer(mine), 1)
             cx.rt.recv(cx.b, Buffer(got), 1)
@@ -728,21 +780,36 @@ def sc_p2p(cx: Ctx):
             cx.rt.recv(cx.b, Buffer(got), 0)
             cx.rt.send(cx.b, Buffer(mine), 0)
         cx.check("p2p/pingpong", from_dev(got, DType.bf16), y[1 - r])
-    # self-send
+
+
+def _p2p_self(cx):
+    p, r, dev = cx.p, cx.r, cx.dev
     z = values(DType.u8, 9999, "self", r)
     zd = torch.zeros(9999, dtype=torch.uint8, device=dev)
-    cx.rt.send(cx.b, Buffer(to_dev(z, DType.u8, dev)), r)
+    zs = to_dev(z, DType.u8, dev)
+    cx.lockstep(("self",))
+    cx.rt.send(cx.b, Buffer(zs), r)
     cx.rt.recv(cx.b, Buffer(zd), r)
     cx.check("p2p/self", from_dev(zd, DType.u8), z)
-    # staged numpy buffers (reference-style host Buffers)
+
+
+def _p2p_host(cx, nxt, prv):
+    """Staged numpy buffers (reference-style host Buffers)."""
+    p, r, dev = cx.p, cx.r, cx.dev
     hx = [values(DType.i32, 5000, "p2phost", q) for q in range(p)]
     hout = np.zeros(5000, dtype=np.int32)
+    cx.lockstep(("host",))
     cx.rt.send(cx.b, Buffer(hx[r].copy()), nxt)
     cx.rt.recv(cx.b, Buffer(hout), prv)
     cx.check("p2p/host", hout, hx[prv])
-    # CUDA graph: one captured ring shift, replayed with fresh inputs
+
+
+def _p2p_graph(cx, nxt, prv):
+    """CUDA graph: one captured ring shift, replayed with fresh inputs."""
+    p, r, dev = cx.p, cx.r, cx.dev
     gi = torch.zeros(777_777, device=dev)
     go = torch.zeros_like(gi)
+    cx.lockstep(("graph-warmup",))
     cx.rt.send(cx.b, Buffer(gi), nxt)  # warm-up outside the capture
     cx.rt.recv(cx.b, Buffer(go), prv)
     cx.sync()
@@ -760,15 +827,21 @@ def sc_p2p(cx: Ctx):
         cx.sync()
         cx.check(f"p2p/graph{it}", from_dev(go, DType.f32), x[prv])
     del g
-    # LengthMismatch: rank 1 posts one element more than rank 0 sends
+
+
+def _p2p_lenm(cx):
+    """LengthMismatch: rank 1 posts one element more than rank 0 sends."""
+    p, r, dev = cx.p, cx.r, cx.dev
+    lm = torch.ones(100, device=dev) if r == 0 else torch.zeros(101, device=dev)
+    cx.lockstep(("lenm",))
     if p >= 2 and r < 2:
         if r == 0:
-            cx.rt.send("lenm", Buffer(torch.ones(100, device=dev)), 1)
+            cx.rt.send("lenm", Buffer(lm), 1)
             cx.sync()
         else:
             raised = None
             try:
-                cx.rt.recv("lenm", Buffer(torch.zeros(101, device=dev)), 0, async_op=True)
+                cx.rt.recv("lenm", Buffer(lm), 0, async_op=True)
                 cx.rt.synchronize(["lenm"])
             except Exception as exc:  # noqa: BLE001
                 raised = exc
@@ -979,7 +1052,10 @@ def sc_commlog(cx: Ctx):
     if ops != sorted(["all_reduce", "all_to_all_single", "all_reduce"]):
         cx.failures.append(f"commlog: records {ops}")
     for rec in recs:
-        if not (rec.dur_us > 0 and rec.backend == cx.b and rec.rank == r):
+        # at p >= 2 every op runs a kernel that stamps its own device time:
+        # the 0.001 us "no stamps" placeholder is a failure there
+        floor = 0.0011 if p > 1 else 0.0
+        if not (rec.dur_us > floor and rec.backend == cx.b and rec.rank == r):
             cx.failures.append(f"commlog: bad record {rec}")
         want_bytes = {"all_reduce": None, "all_to_all_single": p * 4096 * 4}.get(rec.op)
         if want_bytes is not None and rec.bytes != want_bytes:
@@ -992,6 +1068,211 @@ def sc_commlog(cx: Ctx):
         rows = {(row.op, row.backend): row for row in bd.rows}
         if ("all_reduce", cx.b) not in rows or rows[("all_reduce", cx.b)].count < 2:
             cx.failures.append(f"commlog: report rows {bd.rows}")
+
+
+# ------------------------------------------------------- BASELINE configs
+
+def bits(dtype: DType, n: int, *seed) -> np.ndarray:
+    """Seeded random BIT PATTERNS of `dtype` (movement parity: every pattern,
+    NaN payloads included, must arrive unchanged)."""
+    def make():
+        rng = np.random.default_rng(seed_of("bits", *seed))
+        w = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}[dtype.size_bytes]
+        return rng.integers(0, np.iinfo(w).max, size=n, dtype=w, endpoint=True).view(NP[dtype])
+    if _MEMO is not None:
+        return _MEMO.get(("b", dtype, n, seed), make)
+    return make()
+
+
+def dlrm_counts(p: int, skew: bool):
+    """cfg4: 26 tables of dim 128 split over ranks like
+    np.array_split, global batch 65536; uniform local batch B/p or Zipf(1.1)
+    weights normalized to 65536 (remainder to the last rank).
+    sc[i][j] = b_j * T_i * 128 elements rank i sends to rank j."""
+    tables = [len(x) for x in np.array_split(np.arange(26), p)]
+    B = 65536
+    if skew:
+        wz = [(j + 1) ** -1.1 for j in range(p)]
+        b = [int(B * w / sum(wz)) for w in wz]
+        b[-1] += B - sum(b)
+    else:
+        b = [B // p] * p
+    return [[b[j] * tables[i] * 128 for j in range(p)] for i in range(p)], b
+
+
+def _a2av_case(cx, name, dtype, sc, backend=None, devcounts=True):
+    """all_to_allv with counts matrix sc (sc[i][j]: i -> j), packed displs;
+    host counts and (optionally) device-resident counts, vs the oracle."""
+    p, r = cx.p, cx.r
+    b = backend or cx.b
+    sd = [packed(row) for row in sc]
+    rd = [packed([sc[j][q] for j in range(p)]) for q in range(p)]
+    ins = [bits(dtype, sum(sc[q]), name, q) for q in range(p)]
+    rc = [sc[j][r] for j in range(p)]
+    want = seqref.all_to_allv_rank(ins, sc, sd, rd, r, sum(rc))
+    i = to_dev(ins[r], dtype, cx.dev)
+    o = torch.zeros(sum(rc), dtype=i.dtype, device=cx.dev)
+    cx.rt.all_to_allv(b, Buffer(o), Buffer(i), sc[r], rc, sd[r], rd[r])
+    cx.check(f"{name}/host-counts", from_dev(o, dtype), want)
+    if devcounts:
+        o.zero_()
+        dc = [torch.tensor(v, dtype=torch.int64, device=cx.dev) for v in (sc[r], rc, sd[r], rd[r])]
+        cx.rt.all_to_allv(b, Buffer(o), Buffer(i), dc[0], dc[1], dc[2], dc[3])
+        cx.check(f"{name}/device-counts", from_dev(o, dtype), want)
+    return i, o
+
+
+def sc_baseline(cx: Ctx):
+    """BASELINE.json configs 3-5 at full size through the public API, every
+    output against the oracle: cfg3 DS-MoE token all_to_all,
+    cfg4 DLRM all_to_allv (uniform + Zipf-skewed, host and device counts),
+    cfg5 one mixed step incl. the fusion grouping of the 14 MLP gradients
+    against the reference FusionManager's own grouping (tests/golden/
+    cfg5_fusion.json, oracle/make_golden.py cfg5)."""
+    p, r, dev = cx.p, cx.r, cx.dev
+    # cfg3: 4096 tokens x 4096 hidden bf16 per rank, one expert per rank
+    n = 4096 * 4096
+    ins = [bits(DType.bf16, n, "cfg3", q) for q in range(p)]
+    m = n // p
+    want = np.concatenate([ins[j][r * m:(r + 1) * m] for j in range(p)])
+    x = to_dev(ins[r], DType.bf16, dev)
+    y = torch.zeros_like(x)
+    cx.rt.all_to_all_single(cx.b, Buffer(y), Buffer(x))
+    cx.check("cfg3/all_to_all_single", from_dev(y, DType.bf16), want)
+    del x, y
+    _a2av_case(cx, "cfg3/a2av-uniform", DType.bf16, [[m] * p for _ in range(p)])
+    # cfg4: DLRM embedding all_to_allv, f32
+    for skew in (False, True):
+        sc, _b = dlrm_counts(p, skew)
+        _a2av_case(cx, f"cfg4/{'skew' if skew else 'uniform'}", DType.f32, sc)
+    # cfg5: one mixed step
+    golden = json.loads((ROOT / "tests" / "golden" / "cfg5_fusion.json").read_text())
+    mlp = golden["posting_order_elems"]
+    sc, _b = dlrm_counts(p, False)
+    cx.rt.synchronize(["fused"])
+    n0 = len(cx.rt.comm_log.records())
+    fwd_in, fwd_out = _a2av_case(cx, "cfg5/a2av-fwd", DType.f32, sc, devcounts=False)
+    gin = [[values(DType.f32, k, "cfg5-grad", gi, q) for q in range(p)] for gi, k in enumerate(mlp)]
+    gts = [to_dev(gin[gi][r], DType.f32, dev) for gi in range(len(mlp))]
+    hs = [cx.rt.all_reduce("fused", Buffer(t), async_op=True) for t in gts]
+    agc = [1000 + 137 * q for q in range(p)]
+    agi = [values(DType.i64, agc[q], "cfg5-ag", q) for q in range(p)]
+    ago = torch.zeros(sum(agc), dtype=torch.int64, device=dev)
+    cx.rt.all_gatherv(cx.b, Buffer(ago), Buffer(to_dev(agi[r], DType.i64, dev)), agc, packed(agc))
+    gvc = [16 * (q + 1) for q in range(p)]
+    gvi = [values(DType.f32, gvc[q], "cfg5-gv", q) for q in range(p)]
+    gvo = torch.zeros(sum(gvc), device=dev) if r == 0 else None
+    cx.rt.gatherv(cx.b, Buffer(gvo) if gvo is not None else None,
+                  Buffer(to_dev(gvi[r], DType.f32, dev)), 0, gvc, packed(gvc))
+    # backward: transposed counts, the forward output is the input
+    sct = [[sc[j][i] for j in range(p)] for i in range(p)]
+    bwd = torch.zeros(sum(sc[r]), device=dev)
+    rct = [sct[j][r] for j in range(p)]
+    cx.rt.all_to_allv(cx.b, Buffer(bwd), Buffer(fwd_out), sct[r], rct, packed(sct[r]), packed(rct))
+    for h in hs:
+        cx.rt.wait(h)
+    cx.rt.synchronize([cx.b, "fused"])
+    for gi in range(len(mlp)):
+        cx.check(f"cfg5/grad{gi}/{mlp[gi]}", from_dev(gts[gi], DType.f32), seqref.fold(gin[gi], "sum"))
+    cx.check("cfg5/all_gatherv", from_dev(ago, DType.i64), seqref.all_gatherv(agi, agc, packed(agc))[r])
+    if r == 0:
+        cx.check("cfg5/gatherv", from_dev(gvo, DType.f32), seqref.gatherv(gvi, 0, gvc, packed(gvc))[0])
+    # the backward exchange returns every row to where it started
+    cx.check("cfg5/a2av-bwd-roundtrip", from_dev(bwd, DType.f32), from_dev(fwd_in, DType.f32))
+    recs = sorted((x for x in cx.rt.comm_log.records()[n0:] if x.backend == "fused"),
+                  key=lambda x: x.seq)
+    got = [x.members for x in recs if x.fused]
+    cx.checked += 1
+    if got != golden["flush_members"] or sum(1 for x in recs if not x.fused) != golden["unfused_records"]:
+        cx.failures.append(f"cfg5/fusion grouping: flushes {got} (+{sum(1 for x in recs if not x.fused)} "
+                           f"unfused) vs reference {golden['flush_members']} "
+                           f"(+{golden['unfused_records']})")
+
+
+def _ints_f32(n: int, q: int) -> np.ndarray:
+    """Small-integer f32 values: every partial sum is exact, so any summation
+    order (ascending fold, NVLS switch order) gives the same bits."""
+    i = np.arange(n, dtype=np.int64)
+    return (((i * 31 + q * 17) % 29) - 14).astype(np.float32)
+
+
+def sc_large(cx: Ctx):
+    """all_reduce at the sizes AUTO sends to the large-message kernels:
+    256 MiB f32 / bf16 (two-shot with TMA bulk senders for aligned buffers,
+    NVLS at p >= 4 where the switch exists) and 1 GiB f32 (several launches
+    through the workspace / NVLS halves), against the oracle. 1 GiB uses
+    exactly-summable integer values (any reduction order is bit-exact)."""
+    p, r, dev = cx.p, cx.r, cx.dev
+    inst = cx.rt._instance(cx.b)
+    nvls = bool(inst.comm.caps.nvls_supported)
+    n = (256 << 20) // 4
+    ins = [values(DType.f32, n, "large-f32", q) for q in range(p)]
+    t = to_dev(ins[r], DType.f32, dev)
+    cx.rt.all_reduce(cx.b, Buffer(t))
+    cx.check("large/f32/256MiB", from_dev(t, DType.f32), seqref.fold(ins, "sum"),
+             float_reduction=nvls and p >= 4, rtol=1e-5)
+    del t
+    # misaligned by one element: the same share geometry, LD/ST senders
+    base = torch.zeros(n + 1, device=dev)
+    t = base[1:]
+    t.copy_(torch.from_numpy(ins[r].copy()))
+    cx.rt.all_reduce(cx.b, Buffer(t))
+    cx.check("large/f32/256MiB-misaligned", from_dev(t, DType.f32), seqref.fold(ins, "sum"),
+             float_reduction=nvls and p >= 4, rtol=1e-5)
+    del t, base, ins
+    nb = (256 << 20) // 2
+    ins = [values(DType.bf16, nb, "large-bf16", q) for q in range(p)]
+    t = to_dev(ins[r], DType.bf16, dev)
+    cx.rt.all_reduce(cx.b, Buffer(t))
+    if nvls and p >= 4:
+        cx.check("large/bf16/256MiB", seqref.bf16_bits_to_f32(from_dev(t, DType.bf16)),
+                 seqref.bf16_bits_to_f32(seqref.fold_bf16(ins, "sum")), float_reduction=True,
+                 rtol=1e-2)
+    else:
+        cx.check("large/bf16/256MiB", from_dev(t, DType.bf16), seqref.fold_bf16(ins, "sum"))
+    del t, ins
+    if p <= 4:
+        n = (1 << 30) // 4
+        t = torch.from_numpy(_ints_f32(n, r)).to(dev)
+        cx.rt.all_reduce(cx.b, Buffer(t))
+        acc = _ints_f32(n, 0)
+        for q in range(1, p):
+            acc += _ints_f32(n, q)
+        cx.check("large/f32/1GiB", from_dev(t, DType.f32), acc)
+        del t, acc
+
+
+def sc_tuning(cx: Ctx):
+    """The tuning table drives AUTO (mcrdl_comm_set_tuning): editing the
+    table's all_reduce cell changes the kernel the C layer launches, results
+    stay bit-exact, and restoring the shipped table restores its choice."""
+    from paper_2303_08374_b200.dispatch import TuningTable
+
+    p, r, dev = cx.p, cx.r, cx.dev
+    inst = cx.rt._instance(cx.b)
+    if p < 2:
+        return
+    for algo in ("two_shot", "one_shot", "two_shot"):
+        t = TuningTable.from_dict({"tables": {"all_reduce": {str(p): [
+            {"max_bytes": 1 << 40, "backend": "nvl", "algorithm": algo}]}}})
+        inst.install_tuning(t)
+        for n in (1000, 300_001):
+            ins = [values(DType.f32, n, "tune", algo, n, q) for q in range(p)]
+            x = to_dev(ins[r], DType.f32, dev)
+            cx.rt.all_reduce(cx.b, Buffer(x))
+            cx.check(f"tuning/{algo}/{n}", from_dev(x, DType.f32), seqref.fold(ins, "sum"))
+            got = inst.last_algorithm(CommOpKind.all_reduce)
+            cx.checked += 1
+            if got != algo:
+                cx.failures.append(f"tuning: table says {algo} for {n} f32, C layer ran {got}")
+    inst.install_tuning(cx.rt.algorithm_table)
+    rows = inst.tuning_rows[CommOpKind.all_reduce]
+    if rows:
+        x = torch.ones(1000, device=dev)
+        cx.rt.all_reduce(cx.b, Buffer(x))
+        cx.checked += 1
+        if inst.last_algorithm(CommOpKind.all_reduce) != rows[0][1]:
+            cx.failures.append(f"tuning: shipped table row {rows[0]} not applied")
 
 
 def sc_smoke(cx: Ctx):
@@ -1132,19 +1413,25 @@ SCENARIOS = {
     "codec": sc_codec,
     "commlog": sc_commlog,
     "order_mismatch": sc_order_mismatch,
+    "baseline": sc_baseline,
+    "large": sc_large,
+    "tuning": sc_tuning,
 }
 
 
 def run_rank(rank: int, world: int, device: int, report: str, names, shared=None) -> int:
     torch.cuda.set_device(device)
-    if shared is not None:
-        # every co-located rank issues on its own non-blocking stream (the
-        # legacy default stream would serialize the ranks' kernels)
-        torch.cuda.set_stream(torch.cuda.Stream(device))
     out = {"rank": rank, "failures": [], "checked": 0}
     rt = Runtime(rank=rank, world_size=world)
     rt.local_device = device
     if shared is not None:
+        # Co-located rank: exactly two streams (issue + lane), made up front
+        # in rank order so the ranks' streams land on distinct hardware queues
+        # (a stream sharing a queue with a peer's blocked stream can stall
+        # behind it); the legacy default stream would serialize the ranks.
+        issue, lane = shared.streams[rank]
+        torch.cuda.set_stream(issue)
+        rt.lane_stream = lane
         rt.launch_hook = shared.rendezvous
     cx = None
     try:
@@ -1179,6 +1466,9 @@ def run_rank(rank: int, world: int, device: int, report: str, names, shared=None
             cx.failures.append(f"synchronize: {exc!r}")
         out["failures"] = cx.failures
         out["checked"] = cx.checked
+        if cx.failures:  # what each rank ran last (compare ranks on a failure)
+            out["log_tail"] = [[x.backend, x.op, x.bytes, x.seq, x.algorithm]
+                               for x in rt.comm_log.records()[-40:]]
         out["nvls"] = getattr(cx, "nvls", None)
         out["launches"] = _lib.launch_count()
     except Exception:  # noqa: BLE001
@@ -1211,6 +1501,9 @@ def main() -> int:
             faulthandler.dump_traceback_later(dump, repeat=True)
         _MEMO = _Memo()
         shared = Shared(world, timeout=float(os.environ.get("MCRDL_THREAD_TIMEOUT", "600")))
+        torch.cuda.set_device(device)
+        torch.empty(1, device=f"cuda:{device}")  # primary context current in this thread
+        shared.streams = [(_raw_stream(device), _raw_stream(device)) for _ in range(world)]
         rcs = [1] * world
 
         def body(r):

@@ -133,3 +133,57 @@ def test_parse_sizes():
     assert parse_sizes("8:64") == [8, 16, 32, 64]
     assert parse_sizes("1K,4,1M") == [4, 1024, 1 << 20]
     assert parse_sizes("8:1G")[-1] == 1 << 30
+
+
+# ---------------------------------------------------- shipped algorithm table
+
+def test_shipped_table_drives_auto_rows():
+    """The measured table shipped with the package is the default source of
+    AUTO (Runtime.algorithm_table -> install_tuning -> mcrdl_comm_set_tuning);
+    p = 8 has no sweep yet and takes the nearest measured world's cells."""
+    import json
+
+    from paper_2303_08374_b200 import dispatch
+    from paper_2303_08374_b200.core import CommOpKind
+
+    t = dispatch.default_algorithm_table()
+    assert t is not None
+    rows2 = dispatch.algorithm_rows(t, CommOpKind.all_reduce, 2, "any_name")
+    rows4 = dispatch.algorithm_rows(t, CommOpKind.all_reduce, 4, "any_name")
+    assert [a for _, a in rows2][:1] == ["one_shot"] and rows2[-1][1] == "two_shot"
+    assert [m for m, _ in rows4] == sorted(m for m, _ in rows4)
+    assert dispatch.algorithm_rows(t, CommOpKind.all_reduce, 8, "x") == rows4
+    doc = json.loads(dispatch.SHIPPED_TABLE.read_text())
+    assert "8" in doc["untuned_worlds"]
+
+
+def test_algorithm_rows_respect_backend_names():
+    from paper_2303_08374_b200 import dispatch
+    from paper_2303_08374_b200.core import CommOpKind
+
+    doc = {"tables": {"all_reduce": {"2": [
+        {"max_bytes": 1024, "backend": "mine", "algorithm": "one_shot"},
+        {"max_bytes": 1 << 30, "backend": "mine", "algorithm": "two_shot"}]}}}
+    t = dispatch.TuningTable.from_dict(doc)
+    assert dispatch.algorithm_rows(t, CommOpKind.all_reduce, 2, "mine") == [
+        (1024, "one_shot"), (1 << 30, "two_shot")]
+    # a cell routed to another backend is not this backend's algorithm table
+    assert dispatch.algorithm_rows(t, CommOpKind.all_reduce, 2, "other") == []
+    assert dispatch.algorithm_rows(t, CommOpKind.all_reduce, 1, "mine") == []
+    assert dispatch.algorithm_rows(None, CommOpKind.all_reduce, 2, "mine") == []
+
+
+def test_runtime_algorithm_table_default_and_override(tmp_path, monkeypatch):
+    from paper_2303_08374_b200 import Runtime, dispatch
+
+    monkeypatch.delenv("MCRDL_TUNING_TABLE", raising=False)
+    rt = Runtime(0, 1)
+    assert rt.algorithm_table is not None and rt.tuning_table is None
+    p = tmp_path / "t.json"
+    p.write_text('{"tables": {"all_reduce": {"2": [{"max_bytes": 64, "backend": "nvl", '
+                 '"algorithm": "two_shot"}]}}}')
+    monkeypatch.setenv("MCRDL_TUNING_TABLE", str(p))
+    rt = Runtime(0, 1)
+    assert rt.algorithm_table is rt.tuning_table
+    monkeypatch.setenv("MCRDL_ALGO_TABLE", "off")
+    assert Runtime(0, 1).algorithm_table is None
