@@ -1108,7 +1108,11 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
   const int world = c->world;
   const int64_t half = c->dc.half_bytes;
   const bool vec = ((uintptr_t(in) | uintptr_t(out)) & 15) == 0;
-  if (world == 1) return launch_local_copy(out, in, n * int64_t(sizeof(T)), c->num_sms, stream);
+  // p = 1: AUTO is the local copy; an explicitly requested algorithm runs its
+  // real kernel (no peers: flags and folds degenerate to the own input), so
+  // every kernel can be exercised and profiled on a single GPU.
+  if (world == 1 && algo != MCRDL_ALGO_ONE_SHOT && algo != MCRDL_ALGO_TWO_SHOT)
+    return launch_local_copy(out, in, n * int64_t(sizeof(T)), c->num_sms, stream);
   if (root < 0) {
     mcrdl_status_t sst;
     if (try_ar_symm<T, OP>(c, in, out, n, algo, seq, dt, stream, &sst)) return sst;

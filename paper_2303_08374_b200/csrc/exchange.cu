@@ -130,17 +130,18 @@ struct PeerGeo {
   int64_t rmax;
 };
 
-__device__ __forceinline__ void geo_init(PeerGeo& G, const int64_t* bytes, int world, int rank,
-                                         int s, int gmax, int64_t slot, int64_t ll_max,
-                                         int64_t per_cta, int64_t chunk_min, int64_t wide_min) {
+__device__ __forceinline__ void geo_init(PeerGeo& G, const int64_t* bytes, const int64_t* user,
+                                         int world, int rank, int s, int gmax, int64_t slot,
+                                         int64_t ll_max, int64_t per_cta, int64_t chunk_min,
+                                         int64_t wide_min) {
   const int tid = threadIdx.x;
   if (tid < world) {
-    const int64_t B = bytes[tid];
+    const int64_t B = bytes[tid];  // wire bytes
     const int g = pair_ctas(B, gmax, per_cta, wide_min);
     G.g[tid] = g;
     G.ch[tid] = pair_chunk(B, g, chunk_min);
-    // LL pairs (<= kLLMaxPairBytes, ll.cuh) are moved by CTA 0 of each role.
-    G.R[tid] = (tid != rank && s < g && B > ll_max) ? rounds_for(B, slot) : 0;
+    // LL pairs (<= ll_max USER bytes, as both LL ends decide) move as LL lines.
+    G.R[tid] = (tid != rank && s < g && user[tid] > ll_max) ? rounds_for(B, slot) : 0;
   }
   __syncthreads();
   if (tid == 0) {
@@ -216,7 +217,7 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
   }
   if (tid == 0 && s_sb[rank] != s_rb[rank]) s_err = MCRDL_ERR_VALIDATION;
   __syncthreads();
-  // LL carries small pairs unless the codec is on (LL moves raw bytes)
+  // LL carries small pairs (truncated values when the codec is on)
   const int64_t ll_max = a.ll_max;
   if (s_err) {
     if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
@@ -230,7 +231,8 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
     if (ll_max >= 0)
       exchange_ll_send_pairs(S.pad, rank, world, par, s_sp, s_sb, a.sig_base, epoch, ll_max, s,
                              a.gp);
-    geo_init(G, s_sw, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min, a.wide_min);
+    geo_init(G, s_sw, s_sb, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min,
+             a.wide_min);
     int sent = 0;  // chunks published to peer `me`
     for (int64_t t = 0; t < G.rmax; ++t) {
       if (t > 0) {  // slot reuse: receiver share s consumed round t-1
@@ -291,7 +293,8 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
     if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
     return;
   }
-  geo_init(G, s_rw, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min, a.wide_min);
+  geo_init(G, s_rw, s_rb, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min,
+           a.wide_min);
   int got = 0;  // chunks consumed from peer `me`
   const uint8_t* my_ws = S.ws[rank] + hoff;
   for (int64_t t = 0; t < G.rmax; ++t) {
@@ -365,9 +368,13 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   // values raise ORDER_MISMATCH instead of landing half-written shares.
   ExchangeSpec spg = sp;
   spg.sig_base =
-      mix32(mix32(mix32(sp.sig_base, uint64_t(pair_cta)), uint64_t(chunk_min)), uint64_t(wide_min)) &
-      ~kSigCodecBit;
-  const int64_t ll_max = sp.codec ? -1 : exchange_ll_max();
+      (mix32(mix32(mix32(sp.sig_base, uint64_t(pair_cta)), uint64_t(chunk_min)), uint64_t(wide_min)) &
+       ~kSigCodecBit) |
+      (sp.codec ? kSigCodecBit : 0u);
+  // LL pairs carry the codec too (truncated values in raw LL lines): both
+  // ends pick LL from the pair's user bytes, so a codec disagreement on a
+  // small pair meets a header with the other codec bit -> CODEC_MISMATCH.
+  const int64_t ll_max = exchange_ll_max();
   if (ll_max >= 0 && try_exchange_ll(c, spg, ll_max, stream, &st)) return st;
   XArgs a;
   memset(&a, 0, sizeof(a));
@@ -388,7 +395,7 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   a.pair_cta = pair_cta;
   a.chunk_min = chunk_min;
   a.wide_min = wide_min;
-  a.sig_base = spg.sig_base | (sp.codec ? kSigCodecBit : 0u);
+  a.sig_base = spg.sig_base;
   a.slot = c->dc.half_bytes / c->world / 256 * 256;
   a.gmax = c->num_sms < kMaxBlocks ? c->num_sms : kMaxBlocks;  // 2 roles -> 2 CTAs/SM
   if (a.gmax < 1) a.gmax = 1;
@@ -397,7 +404,16 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   // local copy also spreads over the receiver CTAs.
   int64_t g = 1;
   if (sp.d_counts != nullptr) {
-    g = a.gmax;
+    // counts live on the device: no pair can exceed the larger buffer, so
+    // size for that instead of always the full grid
+    // (pair_ctas is not monotonic: the largest narrow pair below the wide
+    // threshold may need more CTAs than the capacity itself)
+    const int64_t cap = std::max(sp.in_count, sp.out_count) * sp.esize;
+    const int64_t wire = sp.codec ? cap / 2 : cap;
+    const int64_t narrow = a.wide_min > 0 ? std::min(wire, a.wide_min - 1) : wire;
+    g = std::max<int64_t>(pair_ctas(wire, a.gmax, a.pair_cta, a.wide_min),
+                          pair_ctas(narrow, a.gmax, a.pair_cta, a.wide_min));
+    g = std::max<int64_t>(g, std::min<int64_t>(a.gmax, (cap + (1 << 20) - 1) >> 20));
   } else {
     for (int r = 0; r < c->world; ++r) {
       if (r == c->rank) {

@@ -145,7 +145,7 @@ __device__ __forceinline__ void exchange_ll_body(DevComm c, LLArgs a, uint32_t e
     const int j = (rank + k) % world;
     const int64_t B = a.sbytes[j], nu = (B + 7) / 8;
     ll_send(ll_slot(S.pad[j], par, rank), a.sptr[j], B, nu * b / G, nu * (b + 1) / G, b == 0,
-            mix32(a.sig_base, uint64_t(B)), epoch);
+            ll_pair_sig(a.sig_base, B), epoch, (a.sig_base & kSigCodecBit) != 0);
   }
   if (a.sptr[rank] != a.rptr[rank]) {  // local segment
     int64_t lo, hi;
@@ -165,12 +165,13 @@ __device__ __forceinline__ void exchange_ll_body(DevComm c, LLArgs a, uint32_t e
   if (b == 0 && tid < world && tid != rank) {
     uint2 h;
     int e = 0;
-    const uint32_t sig = mix32(a.sig_base, uint64_t(a.rbytes[tid]));
+    const uint32_t sig = ll_pair_sig(a.sig_base, a.rbytes[tid]);
     if (!poll_ll(ll_slot(S.pad[rank], par, tid), epoch, S.pad[rank], c.timeout_ns, h, &e)) {
       atomicCAS(&s_err, 0, e);
     } else if (h.x != sig || h.y != uint32_t(a.rbytes[tid])) {
-      atomicCAS(&s_err, 0, MCRDL_ERR_ORDER_MISMATCH);
-      raise_error(S.pad, world, c.err, MCRDL_ERR_ORDER_MISMATCH, epoch);
+      const int code = h.x != sig ? ll_header_error(h.x, sig) : MCRDL_ERR_ORDER_MISMATCH;
+      atomicCAS(&s_err, 0, code);
+      raise_error(S.pad, world, c.err, code, epoch);
     }
   }
   __syncthreads();

@@ -96,12 +96,27 @@ __device__ __forceinline__ void store8(uint8_t* dst, int64_t u, int64_t B, uint2
   }
 }
 
+// Header signature of an LL pair: the op hash mixed with the pair's byte
+// count, with bit 19 carrying the payload codec (as the bulk pair_sig), so a
+// codec disagreement is told apart from an order mismatch.
+__device__ __forceinline__ uint32_t ll_pair_sig(uint32_t sig_base, int64_t B) {
+  return (mix32(sig_base & ~kSigCodecBit, uint64_t(B)) & ~kSigCodecBit) | (sig_base & kSigCodecBit);
+}
+__device__ __forceinline__ int ll_header_error(uint32_t got, uint32_t want) {
+  return ((got ^ want) == kSigCodecBit) ? MCRDL_ERR_CODEC_MISMATCH : MCRDL_ERR_ORDER_MISMATCH;
+}
+
 // LL-send units [u0, u1) of a B-byte pair; `hdr` also writes the header.
+// trunc: trunc16 codec on an f32 payload (middleware.py:43-75) — each f32
+// keeps its top 16 bits (the LL line carries raw words, so the wire size is
+// unchanged; the values match the compressed bulk path).
 __device__ __forceinline__ void ll_send(uint8_t* slot, const uint8_t* src, int64_t B, int64_t u0,
-                                        int64_t u1, bool hdr, uint32_t sig, uint32_t epoch) {
+                                        int64_t u1, bool hdr, uint32_t sig, uint32_t epoch,
+                                        bool trunc = false) {
+  const uint32_t mask = trunc ? 0xFFFF0000u : 0xFFFFFFFFu;
   for (int64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
     const uint2 v = load8(src, u, B);
-    st_ll(slot + kLLHeader + u * 16, v.x, v.y, epoch);
+    st_ll(slot + kLLHeader + u * 16, v.x & mask, v.y & mask, epoch);
   }
   if (hdr && threadIdx.x == 0) st_ll(slot, sig, uint32_t(B), epoch);
 }
@@ -115,7 +130,8 @@ __device__ __forceinline__ int ll_recv(const uint8_t* slot, uint8_t* dst, int64_
   if (hdr && threadIdx.x == 0) {
     uint2 h;
     if (!poll_ll(slot, epoch, me, tmo, h, &err)) return err;
-    if (h.x != sig || h.y != uint32_t(B)) return MCRDL_ERR_ORDER_MISMATCH;
+    if (h.x != sig) return ll_header_error(h.x, sig);
+    if (h.y != uint32_t(B)) return MCRDL_ERR_ORDER_MISMATCH;
   }
   const int nt = blockDim.x;
   for (int64_t u = u0 + threadIdx.x; u < u1; u += 4 * nt) {
@@ -154,7 +170,7 @@ __device__ __forceinline__ void exchange_ll_send_pairs(Pad* const* pads, int ran
     if (B > ll_max) continue;
     const int64_t nu = (B + 7) / 8;
     ll_send(ll_slot(pads[j], par, rank), sptr[j], B, nu * b / G, nu * (b + 1) / G, b == 0,
-            mix32(sig_base, uint64_t(B)), epoch);
+            ll_pair_sig(sig_base, B), epoch, (sig_base & kSigCodecBit) != 0);
   }
 }
 __device__ __forceinline__ int exchange_ll_recv_pairs(Pad* const* pads, int rank, int world, int par,
@@ -166,7 +182,7 @@ __device__ __forceinline__ int exchange_ll_recv_pairs(Pad* const* pads, int rank
     if (B > ll_max) continue;
     const int64_t nu = (B + 7) / 8;
     const int e = ll_recv(ll_slot(pads[rank], par, i), rptr[i], B, nu * b / G, nu * (b + 1) / G,
-                          b == 0, mix32(sig_base, uint64_t(B)), epoch, pads[rank], tmo);
+                          b == 0, ll_pair_sig(sig_base, B), epoch, pads[rank], tmo);
     if (e) return e;
   }
   return 0;

@@ -542,6 +542,7 @@ class NvlBackendInstance:
                         off, dtype.code, flush_request.op.code,
                         self._algo_code(CommOpKind.all_reduce, off * esz), flush_request.seq,
                         int(lane.cuda_stream)))
+                    self._post_launch(flush_request)
                 except BaseException as exc:
                     self._fail_now(handle, flush_request, exc)
                     raise
@@ -658,6 +659,13 @@ class NvlBackendInstance:
                 and not torch.cuda.is_current_stream_capturing()):  # captures launch nothing
             hook((self.name, req.seq, sub))
 
+    def _post_launch(self, req: CommRequest) -> None:
+        """Runtime.launch_hook again once this op's kernel is enqueued: every
+        rank's kernel of the op sits in the device's queues before any rank
+        enqueues work that waits on it (a stream's next item waits for its
+        kernel and can block a hardware queue the ranks' streams share)."""
+        self._pre_launch(req, sub=-1)
+
     def _launch(self, req: CommRequest, st: _Staging, s: int) -> None:
         lib, c = self.comm.lib, self.comm.handle
         kind, p, rank, seq = req.kind, self.world_size, self.rank, req.seq
@@ -670,7 +678,14 @@ class NvlBackendInstance:
         if self.compression is not None and self.compression.active_for(req) is not None:
             algo |= CODEC_TRUNC16
             req._algorithm += "+trunc16"
-        chk = _lib.check
+        posted = []
+
+        def chk(rc):
+            _lib.check(rc)
+            if not posted:  # the op's (first) kernel is enqueued
+                posted.append(True)
+                self._post_launch(req)
+
         self._last_raw = s
 
         if kind in (CommOpKind.all_reduce, CommOpKind.reduce, CommOpKind.reduce_scatter):

@@ -684,6 +684,7 @@ def sc_graphs(cx: Ctx):
         state = fill(it)
         cx.lockstep(("graph", it))
         g.replay()
+        cx.lockstep(("graph-enqueued", it))
         # an eager op between replays keeps the device epoch in step
         e = [values(DType.i32, 777, "graph-eager", it, q) for q in range(p)]
         t = to_dev(e[r], DType.i32, dev)
@@ -718,6 +719,7 @@ def sc_p2p(cx: Ctx):
         cx.lockstep(("ring", n))
         cx.rt.send(cx.b, Buffer(src), nxt)
         cx.rt.recv(cx.b, Buffer(dst), prv)
+        cx.lockstep(("ring-enqueued", n))
         cx.check(f"p2p/ring/{n}", from_dev(dst, DType.f32), x[prv])
     # 40 sends queued before their receives (eager: headers and slots free)
     if "queued" in parts:
@@ -746,6 +748,7 @@ def _p2p_queued(cx, nxt, prv):
         cx.rt.send(cx.b, Buffer(srcs[k]), nxt)
     for k in range(40):
         cx.rt.recv(cx.b, Buffer(outs[k]), prv)
+    cx.lockstep(("queued-enqueued",))
     for k in range(40):
         cx.check(f"p2p/queued/{k}", from_dev(outs[k], DType.i64), xs[k][prv])
 
@@ -760,6 +763,7 @@ def _p2p_rendezvous(cx, nxt, prv):
     cx.lockstep(("rendezvous",))
     h = cx.rt.recv(cx.b, Buffer(dst), prv, async_op=True)
     cx.rt.send(cx.b, Buffer(src), nxt)
+    cx.lockstep(("rendezvous-enqueued",))
     h.wait()
     torch.cuda.current_stream().wait_stream(cx.rt._instance(cx.b).stream)
     cx.check("p2p/rendezvous", from_dev(dst, DType.f32), x[prv])
@@ -779,6 +783,8 @@ def _p2p_pingpong(cx):
         else:
             cx.rt.recv(cx.b, Buffer(got), 0)
             cx.rt.send(cx.b, Buffer(mine), 0)
+    cx.lockstep(("pingpong-enqueued",))
+    if p >= 2 and r < 2:
         cx.check("p2p/pingpong", from_dev(got, DType.bf16), y[1 - r])
 
 
@@ -790,6 +796,7 @@ def _p2p_self(cx):
     cx.lockstep(("self",))
     cx.rt.send(cx.b, Buffer(zs), r)
     cx.rt.recv(cx.b, Buffer(zd), r)
+    cx.lockstep(("self-enqueued",))
     cx.check("p2p/self", from_dev(zd, DType.u8), z)
 
 
@@ -812,6 +819,7 @@ def _p2p_graph(cx, nxt, prv):
     cx.lockstep(("graph-warmup",))
     cx.rt.send(cx.b, Buffer(gi), nxt)  # warm-up outside the capture
     cx.rt.recv(cx.b, Buffer(go), prv)
+    cx.lockstep(("graph-warmup-enqueued",))
     cx.sync()
     g = torch.cuda.CUDAGraph()
     with cx.exclusive():
@@ -824,6 +832,7 @@ def _p2p_graph(cx, nxt, prv):
         gi.copy_(torch.from_numpy(x[r]))
         cx.lockstep(("p2pgraph", it))
         g.replay()
+        cx.lockstep(("p2pgraph-enqueued", it))
         cx.sync()
         cx.check(f"p2p/graph{it}", from_dev(go, DType.f32), x[prv])
     del g
@@ -1009,19 +1018,21 @@ def sc_codec(cx: Ctx):
     cx.rt.all_to_all_single(b, Buffer(hout), Buffer(ins[r].copy()))
     cx.check("codec/numpy", hout, seqref.all_to_all_single(mine(ins))[r])
     # ranks disagreeing on the codec (rank 0 compresses on "cm"): CodecMismatch
+    # with bulk-sized pairs (flag signatures) and, on a fresh backend, with
+    # LL-sized pairs (LL header signatures)
     if p >= 2:
-        n = p * 100_000  # bulk-sized pairs (the LL path carries no codec)
-        x = torch.ones(n, device=dev)
-        y = torch.zeros(n, device=dev)
-        raised = None
-        try:
-            cx.rt.all_to_all_single("cm", Buffer(y), Buffer(x), async_op=True)
-            cx.rt.synchronize(["cm"])
-        except Exception as exc:  # noqa: BLE001
-            raised = exc
-        cx.checked += 1
-        if type(raised).__name__ != "CodecMismatch":
-            cx.failures.append(f"codec/mismatch: expected CodecMismatch, got {raised!r}")
+        for be, n in (("cm", p * 100_000), ("cm_ll", p * 1000)):
+            x = torch.ones(n, device=dev)
+            y = torch.zeros(n, device=dev)
+            raised = None
+            try:
+                cx.rt.all_to_all_single(be, Buffer(y), Buffer(x), async_op=True)
+                cx.rt.synchronize([be])
+            except Exception as exc:  # noqa: BLE001
+                raised = exc
+            cx.checked += 1
+            if type(raised).__name__ != "CodecMismatch":
+                cx.failures.append(f"codec/mismatch/{n // p}: expected CodecMismatch, got {raised!r}")
 
 
 def sc_commlog(cx: Ctx):
@@ -1276,27 +1287,20 @@ def sc_tuning(cx: Ctx):
 
 
 def sc_smoke(cx: Ctx):
-    """One small invocation of each hot-path family (smoke())."""
+    """One small invocation of each hot-path family (smoke()): LL, one-shot
+    and two-shot all_reduce (explicit algorithms: at p = 1 too they run their
+    real kernels), all_to_allv with host and with device-resident counts."""
     p, r = cx.p, cx.r
-    for algo in ("one_shot", "two_shot"):
-        n = 70001
-        ins = [values(DType.f32, n, "smoke", algo, q) for q in range(p)]
+    inst = cx.rt._instance(cx.b)
+    for algo, n in (("one_shot", 1000), ("one_shot", 70001), ("two_shot", 70001)):
+        ins = [values(DType.f32, n, "smoke", algo, n, q) for q in range(p)]
         t = to_dev(ins[r], DType.f32, cx.dev)
-        cx.rt._instance(cx.b).policy = AlgorithmPolicy({CommOpKind.all_reduce: algo})
+        inst.policy = AlgorithmPolicy({CommOpKind.all_reduce: algo})
         cx.rt.all_reduce(cx.b, Buffer(t))
-        cx.check(f"smoke/all_reduce/{algo}", from_dev(t, DType.f32), seqref.fold(ins, "sum"))
-    cx.rt._instance(cx.b).policy = AlgorithmPolicy()
+        cx.check(f"smoke/all_reduce/{algo}/{n}", from_dev(t, DType.f32), seqref.fold(ins, "sum"))
+    inst.policy = AlgorithmPolicy()
     sc = counts_matrix(p, 5000, "smoke-a2av")
-    sd = [packed(row) for row in sc]
-    rd = [packed([sc[j][q] for j in range(p)]) for q in range(p)]
-    ins = [values(DType.bf16, sum(sc[q]), "smoke-a2av-in", q) for q in range(p)]
-    want = seqref.all_to_allv(ins, sc, sd, rd, out_counts=[sum(sc[j][q] for j in range(p))
-                                                            for q in range(p)])
-    rc = [sc[j][r] for j in range(p)]
-    i = to_dev(ins[r], DType.bf16, cx.dev)
-    o = torch.zeros(sum(rc), dtype=i.dtype, device=cx.dev)
-    cx.rt.all_to_allv(cx.b, Buffer(o), Buffer(i), sc[r], rc, sd[r], rd[r])
-    cx.check("smoke/all_to_allv", from_dev(o, DType.bf16), want[r])
+    _a2av_case(cx, "smoke/all_to_allv", DType.bf16, sc)
 
 
 def sc_golden(cx: Ctx):
@@ -1449,6 +1453,8 @@ def run_rank(rank: int, world: int, device: int, report: str, names, shared=None
                                       compression=CompressionConfig()))
             # "cm": only rank 0 compresses -> CodecMismatch on every rank
             cfgs.append(BackendConfig("cm", workspace_bytes=64 << 20,
+                                      compression=CompressionConfig() if rank == 0 else None))
+            cfgs.append(BackendConfig("cm_ll", workspace_bytes=16 << 20,
                                       compression=CompressionConfig() if rank == 0 else None))
         rt.init(cfgs)
         cx = Ctx(rt, "nvl", shared)
