@@ -42,6 +42,10 @@ def run_colocated(world: int, scenarios=None, timeout: float = 600.0, extra_env=
                 # every rank's streams map onto the device's hardware queues;
                 # more queues = fewer streams of different ranks sharing one
                 "CUDA_DEVICE_MAX_CONNECTIONS": "32"})
+    if scenarios and "p2p" not in scenarios:
+        # no send/recv in this run: no point-to-point mailboxes (every rank's
+        # communicators share this GPU's memory)
+        env.setdefault("MCRDL_P2P_BYTES", "0")
     env.update(extra_env or {})
     cmd = [sys.executable, str(ROOT / "tests" / "gpu_worker.py"), "--threads", str(world), str(tmp)]
     if scenarios:

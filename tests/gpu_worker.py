@@ -1286,6 +1286,95 @@ def sc_tuning(cx: Ctx):
             cx.failures.append(f"tuning: shipped table row {rows[0]} not applied")
 
 
+A3_KINDS = ("all_reduce", "all_gather", "bcast", "all_to_all_single", "reduce_scatter")
+
+
+def sc_a3(cx: Ctx):
+    """Reference acceptance A3 (test_acceptance.py:160-243) on the device:
+    seeded mixed programs of 3-8 ASYNC collectives spread over two backends,
+    waited for in a shuffled order, then synchronize; every result checked
+    against the oracle and every program bounded in time (no deadlock). Then
+    injected order mismatches: one rank posts bcast where the others post
+    all_reduce at the same sequence number -> every rank raises OrderMismatch
+    (the device restatement of the header agreement, collectives.py:178-285),
+    none hangs."""
+    import random
+    import time
+
+    p, r, dev = cx.p, cx.r, cx.dev
+    n_programs = int(os.environ.get("MCRDL_A3_PROGRAMS", "200"))
+    slow = []
+    for seed in range(n_programs):
+        rng = random.Random(seed)
+        ops = [(rng.choice(A3_KINDS), rng.choice(["a3a", "a3b"]), rng.choice([1, 4, 32]),
+                seed * 1000 + i) for i in range(rng.randint(3, 8))]
+        order = list(range(len(ops)))
+        rng.shuffle(order)
+        t0 = time.monotonic()
+        hs, checks = [], []
+        for kind, be, c, sd in ops:
+            if kind == "all_reduce":
+                ins = [values(DType.i64, c, "a3", sd, q) for q in range(p)]
+                t = to_dev(ins[r], DType.i64, dev)
+                hs.append(cx.rt.all_reduce(be, Buffer(t), async_op=True))
+                checks.append((t, seqref.fold(ins, "sum")))
+            elif kind == "all_gather":
+                ins = [values(DType.i64, c, "a3", sd, q) for q in range(p)]
+                o = torch.zeros(p * c, dtype=torch.int64, device=dev)
+                hs.append(cx.rt.all_gather(be, Buffer(o), Buffer(to_dev(ins[r], DType.i64, dev)),
+                                           async_op=True))
+                checks.append((o, seqref.all_gather(ins)[r]))
+            elif kind == "bcast":
+                root = sd % p
+                ins = [values(DType.i64, c, "a3", sd, q) for q in range(p)]
+                t = to_dev(ins[r], DType.i64, dev)
+                hs.append(cx.rt.bcast(be, Buffer(t), root, async_op=True))
+                checks.append((t, ins[root]))
+            elif kind == "all_to_all_single":
+                ins = [values(DType.i64, p * c, "a3", sd, q) for q in range(p)]
+                o = torch.zeros(p * c, dtype=torch.int64, device=dev)
+                hs.append(cx.rt.all_to_all_single(be, Buffer(o), Buffer(to_dev(ins[r], DType.i64, dev)),
+                                                  async_op=True))
+                checks.append((o, seqref.all_to_all_single(ins)[r]))
+            else:
+                ins = [values(DType.i64, p * c, "a3", sd, q) for q in range(p)]
+                o = torch.zeros(c, dtype=torch.int64, device=dev)
+                hs.append(cx.rt.reduce_scatter(be, Buffer(o), Buffer(to_dev(ins[r], DType.i64, dev)),
+                                               async_op=True))
+                checks.append((o, seqref.reduce_scatter(ins, "sum")[r]))
+        for idx in order:
+            cx.rt.wait(hs[idx])
+        cx.rt.synchronize(["a3a", "a3b"])
+        if time.monotonic() - t0 > 10.0:
+            slow.append(seed)
+        for k, (got, want) in enumerate(checks):
+            cx.check(f"a3/program{seed}/op{k}/{ops[k][0]}", from_dev(got, DType.i64), want)
+    cx.checked += 1
+    if slow:
+        cx.failures.append(f"a3: programs over the 10 s budget: {slow[:10]}")
+    if p < 2:
+        return
+    for trial in range(5):  # injected mismatches, one fresh backend per trial
+        be = f"inj{trial}"
+        victim = trial % p
+        buf = torch.ones(1, device=dev)
+        raised = None
+        t0 = time.monotonic()
+        try:
+            if r == victim:
+                cx.rt.bcast(be, Buffer(buf), victim, async_op=True)
+            else:
+                cx.rt.all_reduce(be, Buffer(buf), async_op=True)
+            cx.rt.synchronize([be])
+        except Exception as exc:  # noqa: BLE001
+            raised = exc
+        cx.checked += 1
+        if type(raised).__name__ != "OrderMismatch":
+            cx.failures.append(f"a3/injection{trial}: expected OrderMismatch, got {raised!r}")
+        elif time.monotonic() - t0 > 30.0:
+            cx.failures.append(f"a3/injection{trial}: verdict took {time.monotonic() - t0:.1f} s")
+
+
 def sc_smoke(cx: Ctx):
     """One small invocation of each hot-path family (smoke()): LL, one-shot
     and two-shot all_reduce (explicit algorithms: at p = 1 too they run their
@@ -1420,6 +1509,7 @@ SCENARIOS = {
     "baseline": sc_baseline,
     "large": sc_large,
     "tuning": sc_tuning,
+    "a3": sc_a3,
 }
 
 
@@ -1443,6 +1533,10 @@ def run_rank(rank: int, world: int, device: int, report: str, names, shared=None
                                                                                max_wait=5.0))]
         if "order_mismatch" in names:
             cfgs.append(BackendConfig("mism", workspace_bytes=8 << 20))
+        if "a3" in names:
+            cfgs += [BackendConfig("a3a", workspace_bytes=8 << 20),
+                     BackendConfig("a3b", workspace_bytes=8 << 20)]
+            cfgs += [BackendConfig(f"inj{k}", workspace_bytes=4 << 20) for k in range(5)]
         if "all_to_allv" in names:
             cfgs.append(BackendConfig("small", workspace_bytes=16 << 20))
         if "p2p" in names:
