@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import datetime
+import os
 from typing import List, Optional
 
 from ..errors import BootstrapTimeout
@@ -69,6 +70,9 @@ def make_store(rank: int, world: int, addr: str, port: int, timeout: float):
         raise BootstrapTimeout(
             "world > 1 needs a rendezvous port: set MCRDL_MASTER_PORT (or MASTER_PORT) or "
             "pass master_port to Runtime/BackendConfig")
-    return dist.TCPStore(addr, int(port), world, rank == 0,
+    # MCRDL_STORE_EXTERNAL=1: another process (a launcher) hosts the store and
+    # every rank is a client (e.g. rank 0 runs under a profiler)
+    external = os.environ.get("MCRDL_STORE_EXTERNAL", "0") not in ("", "0")
+    return dist.TCPStore(addr, int(port), world, rank == 0 and not external,
                          timeout=datetime.timedelta(seconds=max(timeout, 1.0)),
                          wait_for_workers=False)

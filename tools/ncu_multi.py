@@ -87,12 +87,20 @@ def main() -> int:
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
+    import datetime
+
+    import torch.distributed as dist
+
+    # the launcher hosts the rendezvous store: rank 0 runs under ncu, whose
+    # start-up would otherwise stall the store every rank connects to
+    store = dist.TCPStore("127.0.0.1", port, a.world + 1, True,
+                          timeout=datetime.timedelta(seconds=300), wait_for_workers=False)
     procs = []
     out = Path(a.out)
     for r in range(a.world):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(a.world), LOCAL_RANK=str(r),
                    MCRDL_MASTER_ADDR="127.0.0.1", MCRDL_MASTER_PORT=str(port),
-                   MCRDL_TIMEOUT_SECS="120")
+                   MCRDL_STORE_EXTERNAL="1", MCRDL_TIMEOUT_SECS="120")
         cmd = [sys.executable, __file__, "--rank-main", "--reps", str(a.reps)]
         if r == 0:
             cmd = ["ncu", "--metrics", a.metrics, "--clock-control", "none",
@@ -100,6 +108,7 @@ def main() -> int:
                    "--log-file", str(out) + ".csv"] + cmd
         procs.append(subprocess.Popen(cmd, env=env))
     rcs = [p.wait() for p in procs]
+    del store
     print("rcs", rcs)
     rows = list(csv.DictReader(open(str(out) + ".csv")))
     summary: dict = {}
