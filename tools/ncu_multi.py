@@ -110,9 +110,11 @@ def main() -> int:
     rcs = [p.wait() for p in procs]
     del store
     print("rcs", rcs)
-    rows = list(csv.DictReader(open(str(out) + ".csv")))
+    lines = open(str(out) + ".csv").read().splitlines()
+    start = next((i for i, ln in enumerate(lines) if ln.startswith('"ID"')), len(lines))
+    rows = list(csv.DictReader(lines[start:]))
     summary: dict = {}
-    for row in rows[1:] if rows and rows[0].get("ID") == "" else rows:
+    for row in rows[1:] if rows and rows[0].get("ID") == "" else rows:  # raw page: units row
         name = row.get("Kernel Name", "?").split("(")[0]
         rec = {k: row[k] for k in row if any(m.split(".")[0] in k for m in a.metrics.split(","))}
         summary.setdefault(name, []).append(rec)
