@@ -4,11 +4,15 @@
 // np.concatenate (middleware.py:316) and _scatter_back copies each member's
 // slice out again (middleware.py:329-341). On the device both are one launch
 // over a segment table; the fused all_reduce (allreduce.cu, k_ar_fused)
-// removes them from the hot path entirely, these remain for the two-shot
-// (large fusion buffer) path and as standalone C-ABI entry points.
+// removes them from the hot path for groups whose one-shot slots fit a
+// workspace half; larger groups (nvl/backend.py post_fused) pack, run the
+// two-shot / NVLS all_reduce on the packed buffer, and unpack.
 #include "internal.h"
 
 namespace mcrdl {
+
+// CTAs per member: members are at most one fusion buffer (FusionConfig B)
+constexpr int kFusionCtasPerMember = 32;
 
 // grid.y = segment, grid.x = CTA share of that segment.
 __global__ void __launch_bounds__(kThreads)
@@ -37,7 +41,7 @@ mcrdl_status_t mcrdl_fusion_pack(const void* const* d_src_ptrs, const int64_t* d
                                  const int64_t* d_offsets, int n, void* dst, void* stream) {
   if (n <= 0) return MCRDL_OK;
   if (n > 65535) return set_error(MCRDL_ERR_VALIDATION, "too many fusion members (%d)", n);
-  dim3 grid(4, n);
+  dim3 grid(kFusionCtasPerMember, n);
   k_pack<<<grid, kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const uint8_t* const*>(d_src_ptrs), d_nbytes, d_offsets,
       reinterpret_cast<uint8_t*>(dst));
@@ -50,7 +54,7 @@ mcrdl_status_t mcrdl_fusion_unpack(const void* src, void* const* d_dst_ptrs, con
                                    const int64_t* d_offsets, int n, void* stream) {
   if (n <= 0) return MCRDL_OK;
   if (n > 65535) return set_error(MCRDL_ERR_VALIDATION, "too many fusion members (%d)", n);
-  dim3 grid(4, n);
+  dim3 grid(kFusionCtasPerMember, n);
   k_unpack<<<grid, kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const uint8_t*>(src), reinterpret_cast<uint8_t* const*>(d_dst_ptrs), d_nbytes,
       d_offsets);

@@ -531,17 +531,38 @@ class NvlBackendInstance:
                     counts.append(m.input.count)
                     offs.append(off)
                     off += (m.input.count + align - 1) // align * align
-                table = torch.tensor([ins, outs, counts, offs], dtype=torch.int64).pin_memory()
+                nbytes = [c * esz for c in counts]
+                offb = [o * esz for o in offs]
+                table = torch.tensor([ins, outs, counts, offs, nbytes, offb],
+                                     dtype=torch.int64).pin_memory()
                 dtable = table.to(self.device, non_blocking=True)
                 st.keep.extend([table, dtable])
                 n = len(members)
                 base = int(dtable.data_ptr())
+                lib, c, ls = self.comm.lib, self.comm.handle, int(lane.cuda_stream)
+                algo = self._algo_code(CommOpKind.all_reduce, off * esz)
+                # one launch (k_ar_fused: members -> peers' slots, fold, members)
+                # while the group's one-shot slots fit a workspace half; larger
+                # groups: pack kernel -> all_reduce (two-shot / NVLS by AUTO) on
+                # the packed buffer -> unpack kernel (middleware.py:311-344)
+                slot = ((off * esz + 15) // 16 * 16 + 255) // 256 * 256
+                one_launch = slot * self.world_size <= self.comm.caps.workspace_bytes // 2
                 try:
-                    _lib.check(self.comm.lib.mcrdl_all_reduce_fused(
-                        self.comm.handle, base, base + 8 * n, base + 16 * n, base + 24 * n, n,
-                        off, dtype.code, flush_request.op.code,
-                        self._algo_code(CommOpKind.all_reduce, off * esz), flush_request.seq,
-                        int(lane.cuda_stream)))
+                    if one_launch:
+                        _lib.check(lib.mcrdl_all_reduce_fused(
+                            c, base, base + 8 * n, base + 16 * n, base + 24 * n, n, off,
+                            dtype.code, flush_request.op.code, algo, flush_request.seq, ls))
+                    else:
+                        packed = st.scratch(off, dtype)
+                        st.keep.append(packed)
+                        pk = _ptr(packed)
+                        _lib.check(lib.mcrdl_fusion_pack(base, base + 32 * n, base + 40 * n, n, pk,
+                                                         ls))
+                        _lib.check(lib.mcrdl_all_reduce(c, pk, pk, off, dtype.code,
+                                                        flush_request.op.code, algo,
+                                                        flush_request.seq, ls))
+                        _lib.check(lib.mcrdl_fusion_unpack(pk, base + 8 * n, base + 32 * n,
+                                                           base + 40 * n, n, ls))
                     self._post_launch(flush_request)
                 except BaseException as exc:
                     self._fail_now(handle, flush_request, exc)

@@ -598,6 +598,18 @@ def sc_async_and_fusion(cx: Ctx):
     cx.sync()
     for k, t in enumerate(ts):
         cx.check(f"fusion/{k}/{shapes[k]}", from_dev(t, DType.f32), seqref.fold(ins[k], "sum"))
+    # a fusion group whose one-shot slots exceed the workspace half of its
+    # backend ("fused_big": 4 MiB workspace, B = 2 MiB): pack kernel ->
+    # all_reduce on the packed buffer -> unpack kernel
+    shapes = [100_000, 200_000, 150_000, 7]
+    ins = [[values(DType.f32, n, "fusbig", k, q) for q in range(p)] for k, n in enumerate(shapes)]
+    ts = [to_dev(ins[k][r], DType.f32, cx.dev) for k in range(len(shapes))]
+    hs = [cx.rt.all_reduce("fused_big", Buffer(t), ReduceOp.sum, async_op=True) for t in ts]
+    for h in hs:
+        cx.rt.wait(h)
+    cx.sync()
+    for k, t in enumerate(ts):
+        cx.check(f"fusion-packed/{k}/{shapes[k]}", from_dev(t, DType.f32), seqref.fold(ins[k], "sum"))
     # async handles on the plain backend + synchronize
     xs = [values(DType.i32, 10000 + k, "async", k, q) for k in range(6) for q in range(p)]
     ts = [to_dev(xs[k * p + r], DType.i32, cx.dev) for k in range(6)]
@@ -1538,6 +1550,9 @@ def run_rank(rank: int, world: int, device: int, report: str, names, shared=None
                                                                                max_wait=5.0))]
         if "order_mismatch" in names:
             cfgs.append(BackendConfig("mism", workspace_bytes=8 << 20))
+        if "async_fusion" in names:
+            cfgs.append(BackendConfig("fused_big", workspace_bytes=4 << 20,
+                                      fusion=FusionConfig(max_bytes=2 << 20, max_wait=5.0)))
         if "a3" in names:
             cfgs += [BackendConfig("a3a", workspace_bytes=8 << 20),
                      BackendConfig("a3b", workspace_bytes=8 << 20)]
@@ -1566,7 +1581,7 @@ def run_rank(rank: int, world: int, device: int, report: str, names, shared=None
                 cx.failures.append(f"{name}: exception\n{traceback.format_exc()[-3000:]}")
         cx.sync()
         try:
-            rt.synchronize(["nvl", "fused"])
+            rt.synchronize([b for b in ("nvl", "fused", "fused_big") if b in rt.get_backends()])
         except Exception as exc:  # noqa: BLE001
             cx.failures.append(f"synchronize: {exc!r}")
         out["failures"] = cx.failures
