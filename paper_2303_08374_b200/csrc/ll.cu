@@ -250,7 +250,11 @@ bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, int64_t ll_max, cuda
     a.rbytes[r] = sp.rbytes[r];
   }
   a.sig_base = sp.sig_base;
-  int64_t g = (mx / 8 + kLLThreads * 2 - 1) / (kLLThreads * 2);
+  // CTAs: one per kLLThreads * upt units of the widest pair (MCRDL_LL_X_UPT
+  // units per thread, default 2); a function of this rank's own bytes only
+  // (the LL line protocol needs no grid agreement)
+  static const int64_t upt = std::max<int64_t>(1, env_int("MCRDL_LL_X_UPT", 2));
+  int64_t g = (mx / 8 + kLLThreads * upt - 1) / (kLLThreads * upt);
   g = std::max<int64_t>(g, (sp.sbytes[c->rank] + (256 << 10) - 1) >> 18);
   g = std::max<int64_t>(1, std::min<int64_t>(g, std::min(64, 4 * c->num_sms)));
   k_exchange_ll<<<int(g), kLLThreads, 0, stream>>>(c->dc, a);

@@ -49,6 +49,7 @@ def rank_main(reps: int) -> None:
     torch.cuda.set_device(rank)
     rt = Runtime(rank, world)
     rt.init([BackendConfig("nvl")])
+    print(f"rank {rank}/{world}: comm up (pid {os.getpid()})", flush=True)
     inst = rt._instance("nvl")
     kinds = {"all_reduce": CommOpKind.all_reduce, "all_to_all_single": CommOpKind.all_to_all_single,
              "bcast": CommOpKind.bcast}
@@ -69,6 +70,7 @@ def rank_main(reps: int) -> None:
         if rank == 0:
             print(f"OPDONE {tag}", flush=True)
     rt.synchronize()
+    print(f"rank {rank}: all ops done", flush=True)
     rt.close()
 
 
@@ -100,16 +102,20 @@ def main() -> int:
     for r in range(a.world):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(a.world), LOCAL_RANK=str(r),
                    MCRDL_MASTER_ADDR="127.0.0.1", MCRDL_MASTER_PORT=str(port),
-                   MCRDL_STORE_EXTERNAL="1", MCRDL_TIMEOUT_SECS="120")
+                   MCRDL_STORE_EXTERNAL="1", MCRDL_TIMEOUT_SECS="120", MCRDL_DEBUG="1")
         cmd = [sys.executable, __file__, "--rank-main", "--reps", str(a.reps)]
-        if r == 0:
-            cmd = ["ncu", "--metrics", a.metrics, "--clock-control", "none",
+        if r == 0 and not os.environ.get("NCU_MULTI_NO_NCU"):
+            cmd = ["ncu", "--target-processes", "application-only", "--metrics", a.metrics,
+                   "--clock-control", "none",
                    "--kernel-name", "regex:mcrdl", "--csv", "--page", "raw",
                    "--log-file", str(out) + ".csv"] + cmd
-        procs.append(subprocess.Popen(cmd, env=env))
+        log = open(f"{out}.rank{r}.log", "w")
+        procs.append(subprocess.Popen(cmd, env=env, stdout=log, stderr=subprocess.STDOUT))
     rcs = [p.wait() for p in procs]
     del store
     print("rcs", rcs)
+    if not Path(str(out) + ".csv").exists():
+        return 0 if all(rc == 0 for rc in rcs) else 1
     lines = open(str(out) + ".csv").read().splitlines()
     start = next((i for i, ln in enumerate(lines) if ln.startswith('"ID"')), len(lines))
     rows = list(csv.DictReader(lines[start:]))
