@@ -154,12 +154,16 @@ mcrdl_status_t mcrdl_comm_status(mcrdl_comm* comm);
 
 /* Device-timed op log (CommLog durations: the reference appends one record
  * per completed op, runtime.py:209-230, middleware.py:100-124). Every kernel
- * launch stamps %globaltimer at entry and exit into a host-mapped ring — no
- * stream commands, no host sync. mcrdl_comm_log_id returns the id of the last
+ * launch stamps %globaltimer at entry and exit into a ring in device memory —
+ * no stream commands, no host sync — and every 64th launch mirrors the last 64
+ * entries to a host-mapped copy. mcrdl_comm_log_id returns the id of the last
  * launch issued (an op that launched kernels first..last); mcrdl_comm_op_time
- * sets *ns to end(last) - start(first), -1 while not finished, -2 when the
- * 4096-entry ring moved past it. Launches inside a CUDA-graph capture are not
- * logged. */
+ * sets *ns to end(last) - start(first) from the host copy, -1 while not
+ * (yet) mirrored, -2 when the 4096-entry ring moved past it;
+ * mcrdl_comm_log_flush mirrors the whole ring now (host-synchronous: call it
+ * once the communicator's work has completed). Launches inside a CUDA-graph
+ * capture are not logged. */
+mcrdl_status_t mcrdl_comm_log_flush(mcrdl_comm* comm);
 uint64_t mcrdl_comm_log_id(const mcrdl_comm* comm);
 mcrdl_status_t mcrdl_comm_op_time(const mcrdl_comm* comm, uint64_t first, uint64_t last,
                                   int64_t* ns);

@@ -781,6 +781,29 @@ mcrdl_status_t mcrdl_debug_trace(mcrdl_comm* c, uint64_t** host_ptr, uint64_t* s
 
 uint64_t mcrdl_comm_log_id(const mcrdl_comm* c) { return c ? c->log_seq : 0; }
 
+}  // extern "C"
+
+namespace mcrdl {
+__global__ void k_oplog_flush(const Pad* pad, uint64_t* host) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kOpLogSlots * 2; i += gridDim.x * blockDim.x)
+    host[i] = reinterpret_cast<const volatile uint64_t*>(pad->oplog)[i];
+}
+}  // namespace mcrdl
+
+extern "C" {
+
+mcrdl_status_t mcrdl_comm_log_flush(mcrdl_comm* c) {
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  if (c->oplog_host == nullptr || c->log_seq == 0) return MCRDL_OK;
+  void* s = nullptr;
+  mcrdl_status_t st = mcrdl_comm_stream(c, 0, &s);
+  if (st != MCRDL_OK) return st;
+  k_oplog_flush<<<16, 512, 0, reinterpret_cast<cudaStream_t>(s)>>>(c->dc.self, c->dc.oplog);
+  MCRDL_CUDA_CHECK(cudaGetLastError());
+  MCRDL_CUDA_CHECK(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(s)));
+  return MCRDL_OK;
+}
+
 mcrdl_status_t mcrdl_comm_op_time(const mcrdl_comm* c, uint64_t first, uint64_t last, int64_t* ns) {
   if (c == nullptr || ns == nullptr) return set_error(MCRDL_ERR_VALIDATION, "NULL argument");
   *ns = -1;

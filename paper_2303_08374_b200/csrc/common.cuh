@@ -29,6 +29,11 @@ namespace mcrdl {
 
 constexpr int kMaxRanks = MCRDL_MAX_RANKS;
 constexpr int kMaxBlocks = 512;  // flag slots per parity
+// Device-timed op log (CommLog durations): a ring of {start, end} stamps in
+// the pad, mirrored to a host-mapped copy every kOpLogFlush ops by the op's
+// own last CTA and fully by mcrdl_comm_log_flush.
+constexpr int kOpLogSlots = 4096;
+constexpr int kOpLogFlush = 64;
 constexpr int kThreads = 512;
 // Point-to-point mailboxes (p2p.cu): every rank owns one ring of kP2PSlots x
 // kP2PChunk bytes per sender; kP2PHdr message headers per sender.
@@ -64,6 +69,7 @@ struct Pad {
   uint64_t p2p_tx_chunks[kMaxRanks], p2p_tx_msgs[kMaxRanks];
   uint64_t p2p_rx_chunks[kMaxRanks], p2p_rx_msgs[kMaxRanks];
   uint32_t p2p_done[2];  // exit counters of the running send / recv launch
+  uint64_t oplog[kOpLogSlots][2];  // local: {start, end} stamps by log id % slots
 };
 // Region layout: [flag pad | LL area | workspace]. The LL area is written
 // only by LL kernels (ll.cu), so a stale LL line always carries an older
@@ -181,20 +187,32 @@ __device__ __forceinline__ void stage_comm(const DevComm& c, SComm& s) {
 // streams), so launch k+1 always sees launch k's store.
 // Device-timed op log (CommLog durations, reference middleware.py:100-124):
 // block 0 stamps %globaltimer at entry, the last CTA to exit at exit, into a
-// host-mapped ring — no stream commands and no fences (each stamp is ONE
-// 64-bit store: id tag in the top 16 bits, 48-bit ns time below), so logging
-// adds no latency.
-constexpr int kOpLogSlots = 4096;
+// ring in the LOCAL pad (each stamp is ONE 64-bit store: id tag in the top 16
+// bits, 48-bit ns time below). Every kOpLogFlush-th op's last CTA mirrors the
+// last kOpLogFlush entries into the host-mapped ring (the host reads it
+// lazily; mcrdl_comm_log_flush mirrors the rest on demand). Stamping straight
+// into host-mapped memory cost every op its end-of-kernel system-memory flush
+// (0.4-1.8 us measured at p = 2-4, profiles/r2_latency_log_*).
 __device__ __forceinline__ uint64_t oplog_word(uint64_t id) {
   return (id << 48) | (globaltimer_ns() & 0xFFFFFFFFFFFFull);
 }
 __device__ __forceinline__ void oplog_start(const DevComm& c) {
   if (c.log_id != 0 && blockIdx.x == 0 && threadIdx.x == 0)
-    *reinterpret_cast<volatile uint64_t*>(c.oplog + (c.log_id % kOpLogSlots) * 2) = oplog_word(c.log_id);
+    *reinterpret_cast<volatile uint64_t*>(&c.self->oplog[c.log_id % kOpLogSlots][0]) =
+        oplog_word(c.log_id);
 }
 __device__ __forceinline__ void oplog_end(const DevComm& c) {  // last CTA, one thread
-  if (c.log_id != 0)
-    *reinterpret_cast<volatile uint64_t*>(c.oplog + (c.log_id % kOpLogSlots) * 2 + 1) = oplog_word(c.log_id);
+  if (c.log_id == 0) return;
+  *reinterpret_cast<volatile uint64_t*>(&c.self->oplog[c.log_id % kOpLogSlots][1]) =
+      oplog_word(c.log_id);
+  if (c.log_id % kOpLogFlush == 0 && c.oplog != nullptr) {
+    for (uint64_t k = c.log_id + 1 - kOpLogFlush; k <= c.log_id; ++k) {
+      const uint64_t s = k % kOpLogSlots;
+      volatile const uint64_t* src = c.self->oplog[s];
+      c.oplog[s * 2] = src[0];
+      c.oplog[s * 2 + 1] = src[1];
+    }
+  }
 }
 
 __device__ __forceinline__ uint32_t epoch_enter(const DevComm& c) {
@@ -209,6 +227,14 @@ __device__ __forceinline__ uint32_t epoch_enter(const DevComm& c) {
 }
 __device__ __forceinline__ void epoch_exit(const DevComm& c, uint32_t epoch) {
   __syncthreads();
+  if (gridDim.x == 1) {  // one CTA (small messages): no exit counter, no fences —
+    // the kernel boundary orders the store before the comm's next launch
+    if (threadIdx.x == 0) {
+      *reinterpret_cast<volatile uint32_t*>(&c.self->dev_epoch) = epoch;
+      oplog_end(c);
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     __threadfence();
     const uint32_t prev = atomicAdd(&c.self->done_ctas, 1u);

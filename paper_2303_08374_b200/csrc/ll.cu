@@ -251,9 +251,11 @@ bool try_exchange_ll(mcrdl_comm* c, const ExchangeSpec& sp, int64_t ll_max, cuda
   }
   a.sig_base = sp.sig_base;
   // CTAs: one per kLLThreads * upt units of the widest pair (MCRDL_LL_X_UPT
-  // units per thread, default 2); a function of this rank's own bytes only
+  // units per thread, default 1); a function of this rank's own bytes only
   // (the LL line protocol needs no grid agreement)
-  static const int64_t upt = std::max<int64_t>(1, env_int("MCRDL_LL_X_UPT", 2));
+  // (1 measured best at p = 4: 32 / 256 KiB all_to_allv 14.3 / 14.2 us vs
+  // 14.8 / 15.7 with 2, profiles/r2_ll_upt_log_p4.csv)
+  static const int64_t upt = std::max<int64_t>(1, env_int("MCRDL_LL_X_UPT", 1));
   int64_t g = (mx / 8 + kLLThreads * upt - 1) / (kLLThreads * upt);
   g = std::max<int64_t>(g, (sp.sbytes[c->rank] + (256 << 10) - 1) >> 18);
   g = std::max<int64_t>(1, std::min<int64_t>(g, std::min(64, 4 * c->num_sms)));

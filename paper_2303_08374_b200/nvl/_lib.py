@@ -43,6 +43,7 @@ SIGNATURES = {
     "mcrdl_comm_last_algo": (c_int, [_P, c_int]),
     "mcrdl_comm_log_id": (c_uint64, [_P]),
     "mcrdl_comm_op_time": (c_int, [_P, c_uint64, c_uint64, _I64P]),
+    "mcrdl_comm_log_flush": (c_int, [_P]),
     "mcrdl_symm_alloc": (c_int, [_P, c_uint64, POINTER(c_void_p)]),
     "mcrdl_symm_free": (c_int, [_P, _P]),
     "mcrdl_all_reduce": (c_int, [_P, _P, _P, c_uint64, c_int, c_int, c_int, c_uint64, _P]),

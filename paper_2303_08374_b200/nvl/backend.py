@@ -385,6 +385,8 @@ class NvlBackendInstance:
         log = self.runtime.comm_log
         lib, c = self.comm.lib, self.comm.handle
         ns = ctypes.c_int64()
+        if block and self._log_pending:  # the device drained: mirror every stamp now
+            _lib.check(lib.mcrdl_comm_log_flush(c))
         while self._log_pending:
             req, first, last = self._log_pending[0]
             dur = None

@@ -40,7 +40,7 @@ OPS = [
 ]
 
 
-def rank_main(reps: int) -> None:
+def rank_main(reps: int, rnd: int) -> None:
     import torch
 
     from paper_2303_08374_b200 import AlgorithmPolicy, BackendConfig, Buffer, CommOpKind, Runtime
@@ -48,9 +48,10 @@ def rank_main(reps: int) -> None:
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(rank)
     rt = Runtime(rank, world)
-    rt.init([BackendConfig("nvl")])
-    print(f"rank {rank}/{world}: comm up (pid {os.getpid()})", flush=True)
-    inst = rt._instance("nvl")
+    be = f"nvl{rnd}"
+    rt.init([BackendConfig(be)])
+    print(f"rank {rank}/{world} round {rnd}: comm up (pid {os.getpid()})", flush=True)
+    inst = rt._instance(be)
     kinds = {"all_reduce": CommOpKind.all_reduce, "all_to_all_single": CommOpKind.all_to_all_single,
              "bcast": CommOpKind.bcast}
     for tag, op, nbytes, algo in OPS:
@@ -61,11 +62,11 @@ def rank_main(reps: int) -> None:
         inst.policy = AlgorithmPolicy({kinds[op]: algo}) if algo != "auto" else AlgorithmPolicy()
         for _ in range(reps):
             if op == "all_reduce":
-                rt.all_reduce("nvl", Buffer(x))
+                rt.all_reduce(be, Buffer(x))
             elif op == "all_to_all_single":
-                rt.all_to_all_single("nvl", Buffer(y), Buffer(x))
+                rt.all_to_all_single(be, Buffer(y), Buffer(x))
             else:
-                rt.bcast("nvl", Buffer(x), 0)
+                rt.bcast(be, Buffer(x), 0)
         torch.cuda.synchronize()
         if rank == 0:
             print(f"OPDONE {tag}", flush=True)
@@ -82,9 +83,23 @@ def main() -> int:
     ap.add_argument("--metrics", default="gpu__time_duration.sum,dram__bytes_read.sum,"
                                           "dram__bytes_write.sum")
     ap.add_argument("--rank-main", action="store_true")
+    ap.add_argument("--profiled", action="store_true")
     a = ap.parse_args()
     if a.rank_main:
-        rank_main(a.reps)
+        # ncu starts the profiled program twice (an unprofiled first run, then
+        # the profiled one): the profiled rank learns its round from a store
+        # counter, every other rank plays both rounds on fresh backends
+        if a.profiled:
+            import datetime
+
+            import torch.distributed as dist
+
+            st = dist.TCPStore("127.0.0.1", int(os.environ["MCRDL_MASTER_PORT"]), is_master=False,
+                               timeout=datetime.timedelta(seconds=300))
+            rank_main(a.reps, int(st.add("ncu-multi-profiled-run", 1)))
+        else:
+            for rnd in (1, 2):
+                rank_main(a.reps, rnd)
         return 0
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -104,10 +119,11 @@ def main() -> int:
                    MCRDL_MASTER_ADDR="127.0.0.1", MCRDL_MASTER_PORT=str(port),
                    MCRDL_STORE_EXTERNAL="1", MCRDL_TIMEOUT_SECS="120", MCRDL_DEBUG="1")
         cmd = [sys.executable, __file__, "--rank-main", "--reps", str(a.reps)]
-        if r == 0 and not os.environ.get("NCU_MULTI_NO_NCU"):
+        if r == int(os.environ.get("NCU_MULTI_RANK", "0")) and not os.environ.get("NCU_MULTI_NO_NCU"):
+            cmd.append("--profiled")
             cmd = ["ncu", "--target-processes", "application-only", "--metrics", a.metrics,
                    "--clock-control", "none",
-                   "--kernel-name", "regex:mcrdl", "--csv", "--page", "raw",
+                   "--kernel-name", "regex:^k_", "--csv", "--page", "raw",
                    "--log-file", str(out) + ".csv"] + cmd
         log = open(f"{out}.rank{r}.log", "w")
         procs.append(subprocess.Popen(cmd, env=env, stdout=log, stderr=subprocess.STDOUT))
