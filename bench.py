@@ -395,7 +395,12 @@ def run_native(args) -> int:
         line.update(extra)
         traffic = _ncu_traffic(world)
         if traffic is not None:
-            line["roofline"]["traffic"] = traffic
+            line["roofline"]["traffic"] = traffic.get("dram")
+            line["roofline"]["traffic_over_algorithmic"] = (
+                traffic["dram"] / per_launch_bytes if traffic.get("dram") else None)
+            if traffic.get("nvltx") is not None:
+                line["roofline"]["nvlink_tx_bytes"] = traffic["nvltx"]
+            line["roofline"]["traffic_source"] = traffic.get("source")
         print(json.dumps(line), flush=True)
     rt.close()
     if world > 1:
@@ -425,13 +430,17 @@ def autotune(rt, size: int, world: int) -> dict:
 
 
 def _ncu_traffic(world: int):
-    """dram read+write bytes per launch of the dominant kernel from the
-    committed `ncu --set full` capture (profiles/ncu_traffic.json), if any."""
+    """DRAM read+write bytes (and NVLink tx bytes at N > 1) per launch of the
+    dominant kernel from the committed ncu captures (profiles/ncu_traffic.json:
+    `ncu --set full` of k_copy at N = 1, tools/ncu_multi.py at N = 2, 4)."""
     try:
         doc = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
-        return doc.get(str(world))
     except Exception:  # noqa: BLE001
         return None
+    if doc.get(str(world)) is None:
+        return None
+    return {"dram": doc[str(world)], "nvltx": doc.get(f"{world}_nvltx_bytes"),
+            "source": doc.get(f"{world}_source", doc.get("_source"))}
 
 
 def secondary(rt, world, rank, dev, size, barrier, max_over_ranks):

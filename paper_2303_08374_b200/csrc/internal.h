@@ -196,7 +196,11 @@ constexpr int64_t kLLMaxPairBytes = 256 << 10;  // measured: tools/ll_ab.sh, pro
 constexpr int64_t kNvlsFlagBytes = 64 << 10;
 mcrdl_status_t launch_bcast_nvls(mcrdl_comm* c, uint8_t* buf, int64_t nbytes, int root, int dtype,
                                  uint64_t count, uint64_t seq, cudaStream_t stream);
-constexpr int64_t kLLMaxAllReduceBytes = 256 << 10; // all_reduce one-shot message <= this
+// all_reduce one-shot message <= this takes LL lines; above, the bulk one-shot.
+// 128 KiB measured (profiles/r2_ll_threshold_p{2,4}.csv): at 256 KiB the bulk
+// one-shot beats LL (p = 4: 14.0 vs 17.2 us, p = 2: 11.4 vs 11.9), at 128 KiB
+// LL still wins (13.4 vs 13.8, 9.8 vs 10.8).
+constexpr int64_t kLLMaxAllReduceBytes = 128 << 10;
 int64_t exchange_ll_max();
 bool try_exchange_symm(mcrdl_comm* c, const void* in, void* out, uint64_t out_bytes,
                        const int64_t* send_off, const int64_t* recv_off, const int64_t* bytes,
