@@ -1171,7 +1171,8 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
     T* op = out + done;
     const int64_t npk = (m + N - 1) / N;
     if (algo == MCRDL_ALGO_ONE_SHOT && m * int64_t(sizeof(T)) <= ll_max_bytes()) {
-      st = launch_ar_ll<T, OP>(c, ip, op, m, sig, stream);
+      // LL vs bulk one-shot is part of the agreement (MCRDL_LL_MAX_BYTES)
+      st = launch_ar_ll<T, OP>(c, ip, op, m, mix32(sig, 0x4C4Cu) & ~kSigCodecBit, stream);
       if (st != MCRDL_OK) return st;
       done += m;
       ++sub;
