@@ -478,14 +478,17 @@ def secondary(rt, world, rank, dev, size, barrier, max_over_ranks):
         pg = None
         out["nccl_all_reduce"] = {"error": repr(exc)}
 
-    # Same all_reduce on symmetric-memory tensors (Runtime.symmetric_empty):
-    # the zero-copy kernels (NVLS multicast at p >= 3, peer loads at p = 2) —
-    # the opt-in analogue of NCCL user-buffer registration, reported beside
-    # the headline (which uses ordinary tensors).
+    # Same all_reduce on torch tensors allocated in the symmetric MemPool
+    # (Runtime.symmetric_pool, csrc/pool.cu): the zero-copy kernels (NVLS
+    # multicast at p >= 3, peer loads at p = 2) — the analogue of NCCL
+    # user-buffer registration, reported beside the headline (which uses
+    # tensors from torch's default allocator).
     if world > 1:
         try:
-            a_s = rt.symmetric_empty("nvl", size // 4, "f32")
-            o_s = rt.symmetric_empty("nvl", size // 4, "f32")
+            pool = rt.symmetric_pool("nvl", 2 * size + (64 << 20))
+            with torch.cuda.use_mem_pool(pool):
+                a_s = torch.empty(size // 4, device=dev)
+                o_s = torch.empty(size // 4, device=dev)
             a_s.normal_()
             from paper_2303_08374_b200 import CommOpKind, CommRequest, ReduceOp
 
@@ -495,7 +498,8 @@ def secondary(rt, world, rank, dev, size, barrier, max_over_ranks):
             out["all_reduce_symmetric"] = {
                 "busbw_gbs": bus_bytes(world, size) / t / 1e9, "ms": t * 1e3,
                 "frac_of_900": bus_bytes(world, size) / t / 1e9 / 900.0, "bytes_per_rank": size,
-                "path": "k_ar_symm (NVLS multicast)" if world >= 3 else "k_ar_symm (peer loads)"}
+                "path": rt._instance("nvl").last_algorithm(CommOpKind.all_reduce),
+                "tensors": "torch.empty under torch.cuda.use_mem_pool(Runtime.symmetric_pool)"}
         except Exception as exc:  # noqa: BLE001
             out["all_reduce_symmetric"] = {"error": repr(exc)}
 

@@ -30,6 +30,7 @@
 
 #include <stddef.h>
 #include <stdint.h>
+#include <sys/types.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -173,6 +174,21 @@ mcrdl_status_t mcrdl_comm_op_time(const mcrdl_comm* comm, uint64_t first, uint64
  * zero-copy by peers. */
 mcrdl_status_t mcrdl_symm_alloc(mcrdl_comm* comm, uint64_t bytes, void** local_ptr);
 mcrdl_status_t mcrdl_symm_free(mcrdl_comm* comm, void* local_ptr);
+
+/* Symmetric memory pool (csrc/pool.cu): one collective symmetric arena per
+ * pool, sub-allocated first-fit by torch's pluggable-allocator hooks
+ * (torch.cuda.MemPool over mcrdl_pool_malloc / mcrdl_pool_free), so ordinary
+ * framework tensors allocated inside it take the zero-copy paths (k_ar_symm,
+ * k_x_symm) whenever every rank allocates in the same order. mcrdl_pool_create
+ * is collective; mcrdl_pool_activate selects the calling thread's pool for
+ * mcrdl_pool_malloc (NULL: none -> malloc returns NULL). */
+typedef struct mcrdl_pool mcrdl_pool;
+mcrdl_status_t mcrdl_pool_create(mcrdl_comm* comm, uint64_t bytes, mcrdl_pool** pool);
+mcrdl_status_t mcrdl_pool_activate(mcrdl_pool* pool);
+mcrdl_status_t mcrdl_pool_stats(mcrdl_pool* pool, uint64_t* base, uint64_t* bytes, uint64_t* in_use);
+mcrdl_status_t mcrdl_pool_destroy(mcrdl_pool* pool);
+void* mcrdl_pool_malloc(ssize_t size, int device, void* stream);
+void mcrdl_pool_free(void* ptr, size_t size, int device, void* stream);
 
 /* ------------------------------------------------------------ collectives */
 /* `seq` is the reference's per-backend request seq (runtime.py:147-149); it

@@ -21,7 +21,7 @@ CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libmcrdl_nvl.so"
 OBJDIR = ROOT / "build" / "obj"
-SOURCES = ["comm.cu", "allreduce.cu", "exchange.cu", "exchange_api.cu", "fusion.cu", "ll.cu", "p2p.cu", "symm_x.cu"]
+SOURCES = ["comm.cu", "allreduce.cu", "exchange.cu", "exchange_api.cu", "fusion.cu", "ll.cu", "p2p.cu", "symm_x.cu", "pool.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3",
          "-cudart", "static", "--expt-relaxed-constexpr"]

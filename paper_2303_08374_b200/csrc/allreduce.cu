@@ -1076,6 +1076,7 @@ static bool try_ar_symm(mcrdl_comm* c, const T* in, T* out, int64_t n, mcrdl_alg
   uint32_t sig = op_sig(kKindAllReduce, dt, OP, nv ? -3 : -2, uint64_t(n), seq);
   sig = mix32(mix32(sig, oi), oo) & ~kSigCodecBit;
   if ((*st = begin_op(c, stream)) != MCRDL_OK) return true;
+  c->last_algo[MCRDL_TUNE_ALL_REDUCE] = nv ? MCRDL_ALGO_NVLS : MCRDL_ALGO_DIRECT_WRITE;  // zero-copy
   constexpr int N = Pack<T>::N;
   const int64_t shard = ((n + N - 1) / N + c->world - 1) / c->world * 16;  // bytes per rank
   // CTAs: the switch path peaks with ~32 (p = 4: 656 GB/s at 256 MiB vs 566

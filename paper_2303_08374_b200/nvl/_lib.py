@@ -46,6 +46,12 @@ SIGNATURES = {
     "mcrdl_comm_log_flush": (c_int, [_P]),
     "mcrdl_symm_alloc": (c_int, [_P, c_uint64, POINTER(c_void_p)]),
     "mcrdl_symm_free": (c_int, [_P, _P]),
+    "mcrdl_pool_create": (c_int, [_P, c_uint64, POINTER(c_void_p)]),
+    "mcrdl_pool_activate": (c_int, [_P]),
+    "mcrdl_pool_stats": (c_int, [_P, POINTER(c_uint64), POINTER(c_uint64), POINTER(c_uint64)]),
+    "mcrdl_pool_destroy": (c_int, [_P]),
+    "mcrdl_pool_malloc": (c_void_p, [c_int64, c_int, _P]),
+    "mcrdl_pool_free": (None, [_P, c_size_t, c_int, _P]),
     "mcrdl_all_reduce": (c_int, [_P, _P, _P, c_uint64, c_int, c_int, c_int, c_uint64, _P]),
     "mcrdl_reduce_scatter": (c_int, [_P, _P, _P, c_uint64, c_int, c_int, c_int, c_uint64, _P]),
     "mcrdl_reduce": (c_int, [_P, _P, _P, c_uint64, c_int, c_int, c_int, c_int, c_uint64, _P]),

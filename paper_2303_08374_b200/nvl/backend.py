@@ -246,6 +246,7 @@ class NvlBackendInstance:
         self._last_raw: Optional[int] = None  # stream of the most recent op
         self._pool = _PinnedPool()
         self._symm_keep: list = []  # symmetric allocations (freed with the communicator)
+        self._pools: list = []  # (mcrdl_pool handle, torch MemPool)
         self._log_pending: list = []  # (request, first log id, last log id) of inline ops
         n_dev = torch.cuda.device_count()
         dev = config.device if config.device is not None else runtime.local_device
@@ -658,6 +659,25 @@ class NvlBackendInstance:
         self._symm_keep.append(raw)
         return raw[:int(count) * dtype.size_bytes].view(dtype.torch_dtype)
 
+    def symmetric_pool(self, nbytes: int):
+        """Collective (same size, same order on every rank): a torch MemPool
+        whose allocations come from one symmetric arena (csrc/pool.cu). Tensors
+        allocated under `torch.cuda.use_mem_pool(pool)` are ordinary torch
+        tensors that all_reduce / all_to_all take zero-copy (NVLS multimem or
+        peer loads; sender-side direct writes) when every rank allocates them
+        in the same order. The pool serves the calling thread (one rank per
+        thread when ranks are co-located)."""
+        global _POOL_ALLOCATOR
+        h = c_void_p()
+        _lib.check(self.comm.lib.mcrdl_pool_create(self.comm.handle, int(nbytes), byref(h)))
+        _lib.check(self.comm.lib.mcrdl_pool_activate(h))
+        if _POOL_ALLOCATOR is None:
+            _POOL_ALLOCATOR = torch.cuda.memory.CUDAPluggableAllocator(
+                str(_lib.LIB_PATH), "mcrdl_pool_malloc", "mcrdl_pool_free")
+        pool = torch.cuda.MemPool(_POOL_ALLOCATOR.allocator())
+        self._pools.append((h, pool))
+        return pool
+
     def finalize(self, timeout: float) -> None:
         if self.state == "finalized":
             return
@@ -863,6 +883,7 @@ class NvlBackendInstance:
 
 
 _ALGO_NAMES = {v: k for k, v in ALGO_CODES.items()}
+_POOL_ALLOCATOR = None  # torch CUDAPluggableAllocator over mcrdl_pool_malloc/free (one per process)
 CODEC_TRUNC16 = 0x100  # include/mcrdl_nvl.h MCRDL_CODEC_TRUNC16
 
 

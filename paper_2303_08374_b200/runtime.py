@@ -210,6 +210,16 @@ class Runtime:
             raise UnsupportedOperation(f"backend {backend!r} has no symmetric memory")
         return inst.symmetric_empty(count, dtype)
 
+    def symmetric_pool(self, backend: str, nbytes: int):
+        """Collective: a torch.cuda.MemPool over `nbytes` of `backend`'s
+        symmetric memory; tensors allocated under torch.cuda.use_mem_pool(pool)
+        in the same order on every rank take the zero-copy kernels (B200
+        extension)."""
+        inst = self._instance(backend)
+        if not hasattr(inst, "symmetric_pool"):
+            raise UnsupportedOperation(f"backend {backend!r} has no symmetric memory")
+        return inst.symmetric_pool(nbytes)
+
     def get_size(self, backend: str) -> int:
         return self._instance(backend).world_size
 

@@ -1392,6 +1392,42 @@ def sc_a3(cx: Ctx):
             cx.failures.append(f"a3/injection{trial}: verdict took {time.monotonic() - t0:.1f} s")
 
 
+def sc_pool(cx: Ctx):
+    """Runtime.symmetric_pool: ordinary torch tensors allocated in the
+    symmetric MemPool (csrc/pool.cu via torch's pluggable allocator) take the
+    zero-copy kernels — all_reduce in and out of place (k_ar_symm: NVLS
+    multimem where a switch exists, else peer loads), all_to_all_single into a
+    pool output (k_x_symm direct writes) — checked against the oracle."""
+    p, r, dev = cx.p, cx.r, cx.dev
+    pool = cx.rt.symmetric_pool(cx.b, 256 << 20)
+    inst = cx.rt._instance(cx.b)
+    n = (12 << 20) // 4 + 7  # above the zero-copy threshold (8 MiB at p = 2)
+    ins = [values(DType.f32, n, "pool", q) for q in range(p)]
+    m = (6 << 20) // 4  # 6 MiB per pair: inside the direct-write window
+    a2a = [values(DType.i64, p * m // 2, "pool-a2a", q) for q in range(p)]
+    with torch.cuda.use_mem_pool(pool):
+        x = torch.empty(n, device=dev)
+        y = torch.empty(n, device=dev)
+        ai = torch.empty(p * m // 2, dtype=torch.int64, device=dev)
+        ao = torch.empty_like(ai)
+    x.copy_(torch.from_numpy(ins[r].copy()))
+    ai.copy_(torch.from_numpy(a2a[r].copy()))
+    cx.rt.post(CommRequest(CommOpKind.all_reduce, input=Buffer(x), output=Buffer(y),
+                           op=ReduceOp.sum, backend=cx.b))
+    algo = inst.last_algorithm(CommOpKind.all_reduce)
+    cx.check("pool/all_reduce/out", from_dev(y, DType.f32), seqref.fold(ins, "sum"),
+             float_reduction=algo == "nvls", rtol=1e-5)
+    cx.checked += 1
+    if p > 1 and algo not in ("nvls", "direct_write"):
+        cx.failures.append(f"pool: all_reduce on pool tensors ran {algo}, not the zero-copy kernel")
+    cx.rt.all_reduce(cx.b, Buffer(x))
+    cx.check("pool/all_reduce/in", from_dev(x, DType.f32), seqref.fold(ins, "sum"),
+             float_reduction=inst.last_algorithm(CommOpKind.all_reduce) == "nvls", rtol=1e-5)
+    cx.rt.all_to_all_single(cx.b, Buffer(ao), Buffer(ai))
+    cx.check("pool/a2a_single", from_dev(ao, DType.i64), seqref.all_to_all_single(a2a)[r])
+    del x, y, ai, ao
+
+
 def sc_smoke(cx: Ctx):
     """One small invocation of each hot-path family (smoke()): LL, one-shot
     and two-shot all_reduce (explicit algorithms: at p = 1 too they run their
@@ -1527,6 +1563,7 @@ SCENARIOS = {
     "large": sc_large,
     "tuning": sc_tuning,
     "a3": sc_a3,
+    "pool": sc_pool,
 }
 
 

@@ -23,7 +23,7 @@ pytestmark = pytest.mark.gpu
 SCENARIOS = ["golden", "all_reduce", "all_to_allv", "all_to_all", "gathers", "bcast_scatter",
              "reduce_family", "host_buffers", "async_fusion", "graphs", "p2p",
              "symm", "codec", "commlog",
-             "order_mismatch", "baseline", "large", "tuning", "a3"]
+             "order_mismatch", "baseline", "large", "tuning", "a3", "pool"]
 
 
 def _ngpu():
