@@ -700,8 +700,11 @@ mcrdl_status_t mcrdl_comm_init(mcrdl_comm** out, int rank, int world, int cuda_d
   MCRDL_CUDA_CHECK(cudaMemsetAsync(reinterpret_cast<void*>(c->base.ptr[rank]), 0, kPadBytes, kSetupStream));
   MCRDL_CUDA_CHECK(cudaStreamSynchronize(kSetupStream));
 
-  // NVLS buffer: half the workspace size by default; MCRDL_NVLS_BYTES=0 disables.
-  uint64_t nvls_bytes = workspace_bytes / 2;
+  // NVLS buffer: twice the workspace by default (2 GiB halves for the default
+  // 2 GiB workspace), so a 1 GiB all_reduce is ONE k_ar_nvls launch: measured
+  // p = 4, 1 GiB 592 -> 667 GB/s f32 (665 bf16) against two 512 MiB launches
+  // (profiles/r2_nvls_buffer_p4.log). MCRDL_NVLS_BYTES overrides, 0 disables.
+  uint64_t nvls_bytes = 2 * workspace_bytes;
   if (const char* e = getenv("MCRDL_NVLS_BYTES")) nvls_bytes = strtoull(e, nullptr, 10);
   // A multicast object spans distinct GPUs: none for co-located ranks (agreed:
   // every rank computed ranks_per_device from the same UUID table).
