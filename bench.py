@@ -551,50 +551,41 @@ def secondary(rt, world, rank, dev, size, barrier, max_over_ranks):
             res["nccl_error"] = repr(exc)
     out["all_to_allv_dlrm_skew"] = res
 
-    # cfg5 mixed-collective step: a2av forward, the 14 DLRM MLP
-    # gradient all_reduces posted async on the fusion backend (B = 1 MiB,
-    # T = 5 ms), all_gatherv i64 (1000 + 137 r), gatherv f32 -> root 0
-    # (16 (r+1)), a2av backward (transposed counts). Device time per step,
-    # max over ranks, host posting included (the step is what a trainer sees).
+    # cfg5 mixed-collective step, REPLAYED from its LogRecord-
+    # schema JSONL trace (paper_2303_08374_b200/trace.py; the p = 8 trace is
+    # committed as profiles/cfg5_trace_p8.jsonl): a2av forward (cfg4), the 14
+    # DLRM MLP gradient all_reduces posted async on the fusion backend
+    # (B = 1 MiB, T = 5 ms), all_gatherv i64 (1000 + 137 r), gatherv f32 ->
+    # root 0 (16 (r+1)), a2av backward (transposed counts). Device time per
+    # step, max over ranks, host posting included (the step is what a trainer
+    # sees).
     try:
-        mlp = [6656, 512, 262144, 512, 65536, 128, 490496, 1024, 1048576, 1024, 1048576, 1024,
-               1024, 1]
-        grads = [Buffer(torch.randn(k, device=dev)) for k in mlp]
-        agc = [1000 + 137 * q for q in range(world)]
-        agd = [sum(agc[:q]) for q in range(world)]
-        ag_in = Buffer(torch.randint(-1000, 1000, (agc[rank],), dtype=torch.int64, device=dev))
-        ag_out = Buffer(torch.empty(sum(agc), dtype=torch.int64, device=dev))
-        gvc = [16 * (q + 1) for q in range(world)]
-        gvd = [sum(gvc[:q]) for q in range(world)]
-        gv_in = Buffer(torch.randn(gvc[rank], device=dev))
-        gv_out = Buffer(torch.empty(sum(gvc), device=dev))
-        bwd = Buffer(torch.empty(sum(sc), device=dev))
+        import tempfile
+
+        from paper_2303_08374_b200 import trace as tr
+
+        with tempfile.TemporaryDirectory() as d:
+            path = f"{d}/cfg5.jsonl"
+            tr.write_jsonl(tr.cfg5_trace(world), path)
+            recs = tr.load_jsonl(path)
+        rp = tr.Replay(rt, recs, rank, dev)
+        rp.fill(5)
         log = rt.comm_log
-
-        def step():
-            rt.all_to_allv("nvl", O, I, sc, rc, sd, rdp)
-            hs = [rt.all_reduce("nvl_fused", g, async_op=True) for g in grads]
-            rt.all_gatherv("nvl", ag_out, ag_in, agc, agd)
-            rt.gatherv("nvl", gv_out, gv_in, 0, gvc, gvd)
-            rt.all_to_allv("nvl", bwd, O, rc, sc, rdp, sd)
-            for h in hs:
-                rt.wait(h)
-
         reps = 20
         rt.synchronize()
         n0 = len(log.records())
-        t = dev_time(step, reps=reps)
+        t = dev_time(rp.step, reps=reps)
         rt.synchronize()
-        recs = log.records()[n0:]
-        fused = [r_ for r_ in recs if r_.backend == "nvl_fused" and r_.fused]
+        recs_log = log.records()[n0:]
+        fused = [r_ for r_ in recs_log if r_.backend == "nvl_fused" and r_.fused]
         steps_logged = reps + 3  # dev_time's warm-up steps included
         out["mixed_step_cfg5"] = {
-            "step_ms": t * 1e3, "ops_posted_per_step": 18,
+            "step_ms": t * 1e3, "ops_posted_per_step": len(rp.ops),
             "fused_flushes_per_step": len(fused) / steps_logged,
             "fused_members_per_step": sum(r_.members for r_ in fused) / steps_logged,
-            "log_records_per_step": len(recs) / steps_logged,
-            "workload": "cfg5: a2av fwd (cfg4) + 14 MLP-grad all_reduce (fusion B=1MiB, T=5ms) + "
-                        "all_gatherv i64 + gatherv f32 + a2av bwd"}
+            "log_records_per_step": len(recs_log) / steps_logged,
+            "workload": "cfg5 trace replay (LogRecord JSONL): a2av fwd (cfg4) + 14 MLP-grad "
+                        "all_reduce (fusion B=1MiB, T=5ms) + all_gatherv i64 + gatherv f32 + a2av bwd"}
     except Exception as exc:  # noqa: BLE001
         out["mixed_step_cfg5"] = {"error": repr(exc)}
     # DS-MoE cfg3 shape: 4096 tokens x 4096 hidden bf16 per rank, all_to_all_single

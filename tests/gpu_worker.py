@@ -1173,48 +1173,65 @@ def sc_baseline(cx: Ctx):
     for skew in (False, True):
         sc, _b = dlrm_counts(p, skew)
         _a2av_case(cx, f"cfg4/{'skew' if skew else 'uniform'}", DType.f32, sc)
-    # cfg5: one mixed step
+    # cfg5: one mixed step, replayed from its LogRecord-schema JSONL trace
+    # (paper_2303_08374_b200.trace: written, read back, replayed through
+    # Runtime), every output checked, and the fusion flush grouping compared
+    # with the reference FusionManager's on the same posting order
+    import tempfile
+
+    from paper_2303_08374_b200 import trace as tr
+
     golden = json.loads((ROOT / "tests" / "golden" / "cfg5_fusion.json").read_text())
-    mlp = golden["posting_order_elems"]
-    sc, _b = dlrm_counts(p, False)
-    cx.rt.synchronize(["fused"])
-    n0 = len(cx.rt.comm_log.records())
-    fwd_in, fwd_out = _a2av_case(cx, "cfg5/a2av-fwd", DType.f32, sc, devcounts=False)
-    gin = [[values(DType.f32, k, "cfg5-grad", gi, q) for q in range(p)] for gi, k in enumerate(mlp)]
-    gts = [to_dev(gin[gi][r], DType.f32, dev) for gi in range(len(mlp))]
-    hs = [cx.rt.all_reduce("fused", Buffer(t), async_op=True) for t in gts]
-    agc = [1000 + 137 * q for q in range(p)]
-    agi = [values(DType.i64, agc[q], "cfg5-ag", q) for q in range(p)]
-    ago = torch.zeros(sum(agc), dtype=torch.int64, device=dev)
-    cx.rt.all_gatherv(cx.b, Buffer(ago), Buffer(to_dev(agi[r], DType.i64, dev)), agc, packed(agc))
-    gvc = [16 * (q + 1) for q in range(p)]
-    gvi = [values(DType.f32, gvc[q], "cfg5-gv", q) for q in range(p)]
-    gvo = torch.zeros(sum(gvc), device=dev) if r == 0 else None
-    cx.rt.gatherv(cx.b, Buffer(gvo) if gvo is not None else None,
-                  Buffer(to_dev(gvi[r], DType.f32, dev)), 0, gvc, packed(gvc))
-    # backward: transposed counts, the forward output is the input
-    sct = [[sc[j][i] for j in range(p)] for i in range(p)]
-    bwd = torch.zeros(sum(sc[r]), device=dev)
-    rct = [sct[j][r] for j in range(p)]
-    cx.rt.all_to_allv(cx.b, Buffer(bwd), Buffer(fwd_out), sct[r], rct, packed(sct[r]), packed(rct))
-    for h in hs:
-        cx.rt.wait(h)
+    with tempfile.TemporaryDirectory() as d:
+        path = f"{d}/cfg5.jsonl"
+        tr.write_jsonl(tr.cfg5_trace(p), path)
+        recs = tr.load_jsonl(path)
+    rp = tr.Replay(cx.rt, recs, r, dev, backend_map={"nvl": cx.b, "nvl_fused": "fused"})
+    by_rank = {}
+    for rec in recs:
+        by_rank.setdefault(rec["rank"], []).append(rec)
+    for v in by_rank.values():
+        v.sort(key=lambda x: x["seq"])
+    wants = []
+    for i, ent in enumerate(rp.ops):
+        dt = ent["dtype"]
+        peers = [by_rank[q][i] for q in range(p)]
+        if ent["op"] == "all_to_allv":
+            scm = [[int(x) for x in pr["scounts"]] for pr in peers]
+            ins = [bits(dt, sum(scm[q]), "cfg5", i, q) for q in range(p)]
+            want = seqref.all_to_allv_rank(ins, scm, [packed(x) for x in scm],
+                                           [packed([scm[j][q] for j in range(p)]) for q in range(p)],
+                                           r, sum(ent["rc"]))
+            ent["inp"].copy_(to_dev(ins[r], dt, dev))
+            wants.append((ent["out"], want, False))
+        elif ent["op"] == "all_reduce":
+            ins = [values(dt, ent["buf"].numel(), "cfg5", i, q) for q in range(p)]
+            ent["buf"].copy_(to_dev(ins[r], dt, dev))
+            wants.append((ent["buf"], seqref.fold(ins, "sum"), False))
+        else:
+            rc = ent["rc"]
+            ins = [values(dt, rc[q], "cfg5", i, q) for q in range(p)]
+            ent["inp"].copy_(to_dev(ins[r], dt, dev))
+            if ent["op"] == "all_gatherv":
+                wants.append((ent["out"], seqref.all_gatherv(ins, rc, ent["dp"])[r], False))
+            elif r == ent["root"]:
+                wants.append((ent["out"], seqref.gatherv(ins, ent["root"], rc, ent["dp"])[r], False))
+    cx.sync()
     cx.rt.synchronize([cx.b, "fused"])
-    for gi in range(len(mlp)):
-        cx.check(f"cfg5/grad{gi}/{mlp[gi]}", from_dev(gts[gi], DType.f32), seqref.fold(gin[gi], "sum"))
-    cx.check("cfg5/all_gatherv", from_dev(ago, DType.i64), seqref.all_gatherv(agi, agc, packed(agc))[r])
-    if r == 0:
-        cx.check("cfg5/gatherv", from_dev(gvo, DType.f32), seqref.gatherv(gvi, 0, gvc, packed(gvc))[0])
-    # the backward exchange returns every row to where it started
-    cx.check("cfg5/a2av-bwd-roundtrip", from_dev(bwd, DType.f32), from_dev(fwd_in, DType.f32))
-    recs = sorted((x for x in cx.rt.comm_log.records()[n0:] if x.backend == "fused"),
-                  key=lambda x: x.seq)
-    got = [x.members for x in recs if x.fused]
+    n0 = len(cx.rt.comm_log.records())
+    rp.step()
+    cx.rt.synchronize([cx.b, "fused"])
+    for k, (got, want, _) in enumerate(wants):
+        dt = DType.i64 if got.dtype == torch.int64 else DType.f32
+        cx.check(f"cfg5/trace-replay/{k}", from_dev(got, dt), want)
+    recs_log = sorted((x for x in cx.rt.comm_log.records()[n0:] if x.backend == "fused"),
+                      key=lambda x: x.seq)
+    got = [x.members for x in recs_log if x.fused]
+    unfused = sum(1 for x in recs_log if not x.fused)
     cx.checked += 1
-    if got != golden["flush_members"] or sum(1 for x in recs if not x.fused) != golden["unfused_records"]:
-        cx.failures.append(f"cfg5/fusion grouping: flushes {got} (+{sum(1 for x in recs if not x.fused)} "
-                           f"unfused) vs reference {golden['flush_members']} "
-                           f"(+{golden['unfused_records']})")
+    if got != golden["flush_members"] or unfused != golden["unfused_records"]:
+        cx.failures.append(f"cfg5/fusion grouping: flushes {got} (+{unfused} unfused) vs reference "
+                           f"{golden['flush_members']} (+{golden['unfused_records']})")
 
 
 def _ints_f32(n: int, q: int) -> np.ndarray:
