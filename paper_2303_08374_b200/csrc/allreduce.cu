@@ -864,9 +864,13 @@ __global__ void __launch_bounds__(kThreads) k_ar_fused(DevComm c, const T* const
 }
 
 // Local copy used for world == 1 (the p = 1 floor: out[:] = in).
-// Grid-stride (interleaved across CTAs, 8 x 16 B in flight per thread): on
-// B200 this reaches ~93-96% of the measured copy peak where contiguous
-// per-CTA chunks reach ~85% (tools/p2p_probe.cu, tools/copy_probe.cu).
+// One 16 KiB tile per CTA (512 threads x 2 x 16 B, both loads issued before
+// the stores), no grid-stride loop: tools/copy_probe2.cu on B200, 256 MiB back
+// to back: 6.68 TB/s read+write against 5.94 for the former grid-stride
+// kernel (16 x SMs CTAs, whose single-load tail loop ran most of the copy)
+// and 6.38 for cudaMemcpyAsync D2D.
+constexpr int kCopyUnroll = 2;
+constexpr int64_t kCopyTile = int64_t(kThreads) * kCopyUnroll * 16;
 __global__ void __launch_bounds__(kThreads) k_copy(uint8_t* dst, const uint8_t* src, int64_t n) {
   if (((uintptr_t(dst) | uintptr_t(src)) & 15) != 0) {
     int64_t s, e;
@@ -877,17 +881,15 @@ __global__ void __launch_bounds__(kThreads) k_copy(uint8_t* dst, const uint8_t* 
   const int64_t np = n >> 4;
   const uint4* s4 = reinterpret_cast<const uint4*>(src);
   uint4* d4 = reinterpret_cast<uint4*>(dst);
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (; i + 7 * stride < np; i += 8 * stride) {
-    uint4 v[8];
+  const int64_t base = int64_t(blockIdx.x) * (kThreads * kCopyUnroll) + threadIdx.x;
+  uint4 v[kCopyUnroll];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = s4[i + u * stride];
+  for (int u = 0; u < kCopyUnroll; ++u)
+    if (base + u * kThreads < np) v[u] = s4[base + u * kThreads];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) d4[i + u * stride] = v[u];
-  }
-  for (; i < np; i += stride) d4[i] = s4[i];
-  if (blockIdx.x == 0)
+  for (int u = 0; u < kCopyUnroll; ++u)
+    if (base + u * kThreads < np) d4[base + u * kThreads] = v[u];
+  if (blockIdx.x == gridDim.x - 1)
     for (int64_t k = (np << 4) + threadIdx.x; k < n; k += blockDim.x) dst[k] = src[k];
 }
 
@@ -906,11 +908,12 @@ static int grid_for(int64_t packs, int num_sms, int max_blocks) {
 mcrdl_status_t launch_local_copy(void* dst, const void* src, int64_t nbytes, int num_sms,
                                  cudaStream_t stream) {
   if (nbytes <= 0 || dst == src) return MCRDL_OK;
-  // 8 x 16 B in flight per thread over ~16 CTAs per SM measured best for
-  // large copies (tools/copy_probe.cu: 6.32 TB/s vs 6.20 for cudaMemcpy D2D).
-  int64_t g = (nbytes + (int64_t(kThreads) * 128) - 1) / (int64_t(kThreads) * 128);
-  if (g > 16 * num_sms) g = 16 * num_sms;
+  // aligned: one tile per CTA; misaligned: byte shares over 16 CTAs per SM
+  const bool aligned = ((uintptr_t(dst) | uintptr_t(src)) & 15) == 0;
+  int64_t g = aligned ? (nbytes + kCopyTile - 1) / kCopyTile : int64_t(16) * num_sms;
+  if (!aligned && g > (nbytes + 4095) / 4096) g = (nbytes + 4095) / 4096;
   if (g < 1) g = 1;
+  if (g > INT32_MAX) return set_error(MCRDL_ERR_VALIDATION, "local copy too large");
   k_copy<<<int(g), kThreads, 0, stream>>>(reinterpret_cast<uint8_t*>(dst),
                                           reinterpret_cast<const uint8_t*>(src), nbytes);
   count_launch();
