@@ -46,7 +46,6 @@ struct XArgs {
   int64_t pair_cta;  // bytes of a pair per serving CTA (kPairCtaBytes)
   int64_t chunk_min; // minimum flag chunk (kChunkBytes)
   int64_t wide_min;  // pairs of >= wide_min bytes get 4x pair_cta per CTA (0: off)
-  int eager;         // 1: flag (and copy out) each peer's chunk on its own
   uint32_t sig_base;
 };
 
@@ -235,8 +234,6 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
     geo_init(G, s_sw, s_sb, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min,
              a.wide_min);
     int sent = 0;  // chunks published to peer `me`
-    int sent_j[kMaxRanks];  // eager mode, thread 0: chunks published to peer j
-    for (int j = 0; j < kMaxRanks; ++j) sent_j[j] = 0;
     for (int64_t t = 0; t < G.rmax; ++t) {
       if (t > 0) {  // slot reuse: receiver share s consumed round t-1
         if (me < world && t < G.R[me]) {
@@ -261,22 +258,12 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
             block_encode16(dst, s_sp[j] + 2 * (t * slot + lo), hi - lo);
           else
             block_copy<4>(dst, s_sp[j] + t * slot + lo, hi - lo);
-          if (a.eager) {
-            // publish this peer's chunk as soon as it is written: its
-            // receiver copies it out while the next peer's chunk is pushed
-            __syncthreads();
-            if (tid == 0)
-              publish(&S.pad[j]->flag[par][s][rank],
-                      make_flag(epoch, pair_sig(a.sig_base, s_sb[j]), uint32_t(++sent_j[j])));
-          }
         }
-        if (!a.eager) {
-          __syncthreads();
-          if (me < world && me != rank && r < G.n[me]) {
-            ++sent;
-            publish(&S.pad[me]->flag[par][s][rank],
-                    make_flag(epoch, pair_sig(a.sig_base, s_sb[me]), uint32_t(sent)));
-          }
+        __syncthreads();
+        if (me < world && me != rank && r < G.n[me]) {
+          ++sent;
+          publish(&S.pad[me]->flag[par][s][rank],
+                  make_flag(epoch, pair_sig(a.sig_base, s_sb[me]), uint32_t(sent)));
         }
         MCRDL_TRACE_AT(c, bid, 1 + r);
       }
@@ -309,37 +296,9 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
   geo_init(G, s_rw, s_rb, world, rank, s, a.gmax, slot, ll_max, a.pair_cta, a.chunk_min,
            a.wide_min);
   int got = 0;  // chunks consumed from peer `me`
-  int got_i[kMaxRanks];  // eager mode, thread 0: chunks consumed from peer i
-  for (int i = 0; i < kMaxRanks; ++i) got_i[i] = 0;
   const uint8_t* my_ws = S.ws[rank] + hoff;
   for (int64_t t = 0; t < G.rmax; ++t) {
     geo_round(G, s_rw, world, s, slot, t);
-    if (a.eager) {
-      // peers in the order their senders reach this rank (sender q pushes to
-      // q+1, q+2, ...): copy each chunk out as soon as its own flag lands
-      for (int r = 0; r < G.rows; ++r) {
-        for (int k = 1; k < world; ++k) {
-          const int i = (rank - k + world) % world;
-          if (r >= G.n[i]) continue;
-          if (tid == 0) {
-            int e = wait_flag(&S.pad[rank]->flag[par][s][i], S.pad[rank], c.timeout_ns, c.err,
-                              epoch, pair_sig(a.sig_base, s_rb[i]), uint32_t(++got_i[i]));
-            if (e) atomicCAS(&s_err, 0, e);
-          }
-          __syncthreads();
-          if (s_err) {
-            if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
-            return;
-          }
-          const int64_t lo = G.a[i] + r * G.ch[i], hi = min(G.e[i], lo + G.ch[i]);
-          if (a.codec)
-            block_decode16(s_rp[i] + 2 * (t * slot + lo), my_ws + int64_t(i) * slot + lo, hi - lo);
-          else
-            block_copy<4>(s_rp[i] + t * slot + lo, my_ws + int64_t(i) * slot + lo, hi - lo);
-        }
-        MCRDL_TRACE_AT(c, bid, 3 + 2 * r);
-      }
-    } else {
     for (int r = 0; r < G.rows; ++r) {
       if (me < world && me != rank && r < G.n[me]) {
         int e = wait_flag(&S.pad[rank]->flag[par][s][me], S.pad[rank], c.timeout_ns, c.err, epoch,
@@ -363,7 +322,6 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
           block_copy<4>(s_rp[i] + t * slot + lo, my_ws + int64_t(i) * slot + lo, hi - lo);
       }
       MCRDL_TRACE_AT(c, bid, 3 + 2 * r);
-    }
     }
     // Round t of every pair fully landed: let senders reuse the slot.
     if (G.more) {
@@ -437,10 +395,6 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
   a.pair_cta = pair_cta;
   a.chunk_min = chunk_min;
   a.wide_min = wide_min;
-  // Per-peer flags (same flag values as per-row flags, so not part of the
-  // agreement): MCRDL_X_EAGER=0 restores one flag round per row.
-  static const int64_t eager = env_int("MCRDL_X_EAGER", 1);
-  a.eager = eager != 0;
   a.sig_base = spg.sig_base;
   a.slot = c->dc.half_bytes / c->world / 256 * 256;
   a.gmax = c->num_sms < kMaxBlocks ? c->num_sms : kMaxBlocks;  // 2 roles -> 2 CTAs/SM
