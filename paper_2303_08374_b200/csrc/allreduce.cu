@@ -32,12 +32,19 @@ __device__ __forceinline__ void ar_oneshot_body(DevComm c, const T* in, T* out, 
   stage_comm(c, S);
   __syncthreads();
 
-  // Phase 1: each pack read once from HBM, written to p-1 peers.
-  for (int64_t i = pb + tid; i < pe; i += nt) {
-    const uint4 v = load_pack<T, VEC>(in, i, n);
+  // Phase 1: each pack read once from HBM, written to p-1 peers (kBatch
+  // loads in flight per thread before the stores).
+  constexpr int kBatch = 4;
+  for (int64_t i0 = pb + tid; i0 < pe; i0 += kBatch * nt) {
+    uint4 v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (i0 + u * nt < pe) v[u] = load_pack<T, VEC>(in, i0 + u * nt, n);
     for (int k = 1; k < world; ++k) {
-      const int q = (rank + k) % world;
-      st16(S.ws[q] + hoff + int64_t(rank) * slot_bytes + i * 16, v);
+      uint8_t* dst = S.ws[(rank + k) % world] + hoff + int64_t(rank) * slot_bytes;
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u)
+        if (i0 + u * nt < pe) st16(dst + (i0 + u * nt) * 16, v[u]);
     }
   }
   __syncthreads();
@@ -52,16 +59,21 @@ __device__ __forceinline__ void ar_oneshot_body(DevComm c, const T* in, T* out, 
     if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
     return;
   }
-  // Phase 2: ascending fold.
+  // Phase 2: ascending fold; all p loads of a pack are issued before the
+  // first fold (a fold-per-load loop waits one HBM latency per rank).
   const uint8_t* ws = S.ws[rank] + hoff;
   for (int64_t i = pb + tid; i < pe; i += nt) {
+    uint4 raw[kMaxRanks];
+#pragma unroll
+    for (int r = 0; r < kMaxRanks; ++r)
+      if (r < world)
+        raw[r] = (r == rank) ? load_pack<T, VEC>(in, i, n)
+                             : ld16_cg(ws + int64_t(r) * slot_bytes + i * 16);
     Pack<T> acc;
-    acc.from_raw(rank == 0 ? load_pack<T, VEC>(in, i, n) : ld16_cg(ws + i * 16));
-    for (int r = 1; r < world; ++r) {
-      const uint4 v = (r == rank) ? load_pack<T, VEC>(in, i, n)
-                                  : ld16_cg(ws + int64_t(r) * slot_bytes + i * 16);
-      acc.template fold<OP>(v);
-    }
+    acc.from_raw(raw[0]);
+#pragma unroll
+    for (int r = 1; r < kMaxRanks; ++r)
+      if (r < world) acc.template fold<OP>(raw[r]);
     store_pack<T, VEC>(out, i, n, acc.to_raw());
   }
 }
@@ -844,11 +856,14 @@ __device__ __forceinline__ void ar_fused_body(DevComm c, const T* const* in_ptrs
       auto own = [&]() {
         return vec ? load_pack<T, true>(src, li, cnt) : load_pack<T, false>(src, li, cnt);
       };
-      acc.from_raw(rank == 0 ? own() : ld16_cg(ws + i * 16));
-      for (int r = 1; r < world; ++r) {
-        const uint4 v = (r == rank) ? own() : ld16_cg(ws + int64_t(r) * slot_bytes + i * 16);
-        acc.template fold<OP>(v);
-      }
+      uint4 raw[kMaxRanks];  // every rank's pack loaded before the first fold
+#pragma unroll
+      for (int r = 0; r < kMaxRanks; ++r)
+        if (r < world) raw[r] = (r == rank) ? own() : ld16_cg(ws + int64_t(r) * slot_bytes + i * 16);
+      acc.from_raw(raw[0]);
+#pragma unroll
+      for (int r = 1; r < kMaxRanks; ++r)
+        if (r < world) acc.template fold<OP>(raw[r]);
       if (vec) store_pack<T, true>(dst, li, cnt, acc.to_raw());
       else store_pack<T, false>(dst, li, cnt, acc.to_raw());
     }
@@ -1184,11 +1199,18 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
     }
     if (algo == MCRDL_ALGO_ONE_SHOT) {
       const int64_t slot = (npk * 16 + 255) / 256 * 256;
-      const int G = grid_for(npk, c->num_sms, 64);
+      // one pack per thread up to 128 CTAs (profiles/r2_oneshot_geo_ab.csv:
+      // p = 4 8 MiB 61.6 -> 56.8 us, 1 MiB 20.3 -> 19.9 against 64 CTAs x 2
+      // packs; MCRDL_AR_ONESHOT_CTAS / _PPT override)
+      static const int64_t os_ctas = env_int("MCRDL_AR_ONESHOT_CTAS", 128);
+      static const int64_t os_ppt = env_int("MCRDL_AR_ONESHOT_PPT", 1);
+      const int G = grid_for((npk * 2 + os_ppt - 1) / (os_ppt > 0 ? os_ppt : 1), c->num_sms,
+                             int(os_ctas > 0 ? os_ctas : 128));
+      const uint32_t gsig = mix32(sig, uint64_t(G)) & ~kSigCodecBit;  // flags are per CTA
       if (vec)
-        k_ar_oneshot<T, OP, true><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, slot, sig);
+        k_ar_oneshot<T, OP, true><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, slot, gsig);
       else
-        k_ar_oneshot<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, slot, sig);
+        k_ar_oneshot<T, OP, false><<<G, kThreads, 0, stream>>>(c->dc, ip, op, m, slot, gsig);
     } else {
       // CTAs per role: one per 32 KiB of segment; 3 roles x gp <= 2 CTAs/SM
       // (MCRDL_AR_GPMAX / MCRDL_AR_CHUNK_KB override, for tuning).
