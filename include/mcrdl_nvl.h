@@ -257,6 +257,20 @@ mcrdl_status_t mcrdl_all_gatherv(mcrdl_comm* comm, const void* in, void* out,
 mcrdl_status_t mcrdl_gatherv(mcrdl_comm* comm, const void* in, void* out_or_null,
                              const int64_t* rcounts, const int64_t* displs, int root,
                              mcrdl_dtype_t dtype, mcrdl_algo_t algo, uint64_t seq, void* stream);
+/* Device-resident forms of all_gatherv / gatherv (runtime.py:542-569 with
+ * rcounts / displs already on the GPU): d_rcounts and d_displs point to world
+ * int64 each in device memory; the exchange kernel reads them itself (no host
+ * round trip). in_count / out_count (elements) bound every segment; a
+ * violation is latched as MCRDL_ERR_VALIDATION on the device. gatherv: out may
+ * be NULL (out_count ignored) on non-root ranks. */
+mcrdl_status_t mcrdl_all_gatherv_dev(mcrdl_comm* comm, const void* in, uint64_t in_count,
+                                     void* out, uint64_t out_count, const int64_t* d_rcounts,
+                                     const int64_t* d_displs, mcrdl_dtype_t dtype,
+                                     mcrdl_algo_t algo, uint64_t seq, void* stream);
+mcrdl_status_t mcrdl_gatherv_dev(mcrdl_comm* comm, const void* in, uint64_t in_count,
+                                 void* out_or_null, uint64_t out_count, const int64_t* d_rcounts,
+                                 const int64_t* d_displs, int root, mcrdl_dtype_t dtype,
+                                 mcrdl_algo_t algo, uint64_t seq, void* stream);
 /* bcast in place (runtime.py:528-532; collectives.py:418-443). */
 mcrdl_status_t mcrdl_bcast(mcrdl_comm* comm, void* buf, uint64_t count, mcrdl_dtype_t dtype,
                            int root, mcrdl_algo_t algo, uint64_t seq, void* stream);

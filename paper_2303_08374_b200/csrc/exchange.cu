@@ -32,7 +32,10 @@ struct XArgs {
   int64_t sbytes[kMaxRanks];
   uint8_t* rptr[kMaxRanks];
   int64_t rbytes[kMaxRanks];
-  const int64_t* d_counts;  // [scounts | sdispls | rcounts | rdispls] in elements, or null
+  const int64_t* d_counts;  // device counts in elements (layout: d_layout), or null
+  const int64_t* d_displs;  // all_gatherv / gatherv layouts: device displs
+  int d_layout;
+  int d_root;
   const uint8_t* in_base;
   uint8_t* out_base;
   int64_t in_count;  // element capacity of in/out (device-count bounds check)
@@ -195,8 +198,19 @@ __device__ __forceinline__ void exchange_body(DevComm c, XArgs a, uint32_t epoch
   stage_comm(c, S);
   if (tid < world) {
     if (a.d_counts != nullptr) {
-      const int64_t sc = a.d_counts[tid], sd = a.d_counts[world + tid];
-      const int64_t rc = a.d_counts[2 * world + tid], rd = a.d_counts[3 * world + tid];
+      int64_t sc, sd, rc, rd;
+      if (a.d_layout == kDevA2AV) {
+        sc = a.d_counts[tid], sd = a.d_counts[world + tid];
+        rc = a.d_counts[2 * world + tid], rd = a.d_counts[3 * world + tid];
+      } else {
+        // gathers: my block (rcounts[rank]) goes to every receiving peer;
+        // block tid lands at displs[tid] (gatherv: root <-> everyone only)
+        const bool gv = a.d_layout == kDevGatherv;
+        const bool to_peer = !gv || tid == a.d_root;
+        const bool from_peer = !gv || rank == a.d_root;
+        sc = to_peer ? a.d_counts[rank] : 0, sd = 0;
+        rc = from_peer ? a.d_counts[tid] : 0, rd = from_peer ? a.d_displs[tid] : 0;
+      }
       s_sp[tid] = a.in_base + sd * a.esize;
       s_sb[tid] = sc * a.esize;
       s_rp[tid] = a.out_base + rd * a.esize;
@@ -385,6 +399,9 @@ mcrdl_status_t launch_exchange(mcrdl_comm* c, const ExchangeSpec& sp, int64_t to
     a.rbytes[r] = sp.rbytes[r];
   }
   a.d_counts = sp.d_counts;
+  a.d_displs = sp.d_displs;
+  a.d_layout = sp.d_layout;
+  a.d_root = sp.d_root;
   a.in_base = sp.in_base;
   a.out_base = sp.out_base;
   a.in_count = sp.in_count;

@@ -237,6 +237,52 @@ mcrdl_status_t mcrdl_gatherv(mcrdl_comm* c, const void* in, void* out, const int
   return launch_exchange(c, s, total, reinterpret_cast<cudaStream_t>(stream));
 }
 
+// Device-resident rcounts / displs (runtime.py:542-569 with tensors on the
+// GPU): the exchange kernel reads them itself, no host round trip.
+static mcrdl_status_t gather_dev(mcrdl_comm* c, int layout, int kind, const void* in,
+                                 uint64_t in_count, void* out, uint64_t out_count,
+                                 const int64_t* d_rcounts, const int64_t* d_displs, int root,
+                                 mcrdl_dtype_t dtype, mcrdl_algo_t algo, uint64_t seq,
+                                 void* stream) {
+  const int codec = split_codec(&algo, dtype);
+  if (c == nullptr) return set_error(MCRDL_ERR_NOT_INITIALIZED, "communicator is NULL");
+  const int es = elem_size(dtype);
+  if (es == 0) return set_error(MCRDL_ERR_VALIDATION, "unknown dtype %d", int(dtype));
+  if (d_rcounts == nullptr || d_displs == nullptr)
+    return set_error(MCRDL_ERR_VALIDATION, "NULL device count array");
+  if (root < 0 || root >= c->world)
+    return set_error(MCRDL_ERR_VALIDATION, "root %d outside world %d", root, c->world);
+  ExchangeSpec s = empty_spec(es, op_sig(kind, dtype, 2, layout == kDevGatherv ? root : -1, 0, seq));
+  s.codec = codec;
+  s.d_counts = d_rcounts;
+  s.d_displs = d_displs;
+  s.d_layout = layout;
+  s.d_root = root;
+  s.in_base = reinterpret_cast<const uint8_t*>(in);
+  s.out_base = reinterpret_cast<uint8_t*>(out);
+  s.in_count = int64_t(in_count);
+  s.out_count = out == nullptr ? 0 : int64_t(out_count);
+  return launch_exchange(c, s, -1, reinterpret_cast<cudaStream_t>(stream));
+}
+
+mcrdl_status_t mcrdl_all_gatherv_dev(mcrdl_comm* c, const void* in, uint64_t in_count, void* out,
+                                     uint64_t out_count, const int64_t* d_rcounts,
+                                     const int64_t* d_displs, mcrdl_dtype_t dtype,
+                                     mcrdl_algo_t algo, uint64_t seq, void* stream) {
+  return gather_dev(c, kDevAllGatherv, kKindAllGatherv, in, in_count, out, out_count, d_rcounts,
+                    d_displs, 0, dtype, algo, seq, stream);
+}
+
+mcrdl_status_t mcrdl_gatherv_dev(mcrdl_comm* c, const void* in, uint64_t in_count,
+                                 void* out_or_null, uint64_t out_count, const int64_t* d_rcounts,
+                                 const int64_t* d_displs, int root, mcrdl_dtype_t dtype,
+                                 mcrdl_algo_t algo, uint64_t seq, void* stream) {
+  if (c != nullptr && c->rank == root && out_or_null == nullptr)
+    return set_error(MCRDL_ERR_VALIDATION, "root must supply the output buffer");
+  return gather_dev(c, kDevGatherv, kKindGatherv, in, in_count, out_or_null, out_count, d_rcounts,
+                    d_displs, root, dtype, algo, seq, stream);
+}
+
 mcrdl_status_t mcrdl_bcast(mcrdl_comm* c, void* buf, uint64_t count, mcrdl_dtype_t dtype, int root,
                            mcrdl_algo_t algo, uint64_t seq, void* stream) {
   const int codec = split_codec(&algo, dtype);

@@ -179,7 +179,10 @@ struct ExchangeSpec {
   int64_t sbytes[kMaxRanks];
   uint8_t* rptr[kMaxRanks];
   int64_t rbytes[kMaxRanks];
-  const int64_t* d_counts;  // optional device counts (elements)
+  const int64_t* d_counts;  // optional device counts (elements), see d_layout
+  const int64_t* d_displs;  // gather layouts: device displacements (elements)
+  int d_layout;             // kDevA2AV / kDevAllGatherv / kDevGatherv
+  int d_root;               // kDevGatherv: the root
   const uint8_t* in_base;
   uint8_t* out_base;
   int64_t in_count;  // element capacities for device-count bounds checks
@@ -187,6 +190,11 @@ struct ExchangeSpec {
   int esize;
   uint32_t sig_base;
 };
+// Device-resident count layouts the exchange kernel decodes itself:
+//   kDevA2AV:       d_counts = [scounts | sdispls | rcounts | rdispls] (4p)
+//   kDevAllGatherv: d_counts = rcounts (p), d_displs = displs (p)
+//   kDevGatherv:    as all_gatherv, only pairs with d_root carry data
+enum : int { kDevA2AV = 0, kDevAllGatherv = 1, kDevGatherv = 2 };
 mcrdl_status_t launch_exchange(mcrdl_comm* comm, const ExchangeSpec& spec, int64_t total_hint,
                                cudaStream_t stream);
 

@@ -63,6 +63,10 @@ SIGNATURES = {
                                       c_int, c_uint64, _P]),
     "mcrdl_all_gatherv": (c_int, [_P, _P, _P, _I64P, _I64P, c_int, c_int, c_uint64, _P]),
     "mcrdl_gatherv": (c_int, [_P, _P, _P, _I64P, _I64P, c_int, c_int, c_int, c_uint64, _P]),
+    "mcrdl_all_gatherv_dev": (c_int, [_P, _P, c_uint64, _P, c_uint64, _P, _P, c_int, c_int,
+                                      c_uint64, _P]),
+    "mcrdl_gatherv_dev": (c_int, [_P, _P, c_uint64, _P, c_uint64, _P, _P, c_int, c_int, c_int,
+                                  c_uint64, _P]),
     "mcrdl_bcast": (c_int, [_P, _P, c_uint64, c_int, c_int, c_int, c_uint64, _P]),
     "mcrdl_barrier": (c_int, [_P, c_uint64, _P]),
     "mcrdl_send": (c_int, [_P, _P, c_uint64, c_int, _P]),

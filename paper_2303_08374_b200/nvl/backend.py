@@ -794,10 +794,10 @@ class NvlBackendInstance:
             else:
                 counts, displs = req.rcounts, req.rdispls
             if _is_dev(counts) or _is_dev(displs):
-                sc = counts[rank].reshape(1).expand(p)
-                dc = _dev_counts(st, sc, torch.zeros_like(sc), counts, displs)
-                chk(lib.mcrdl_all_to_allv_dev(c, _ptr(i), i.numel(), _ptr(o), o.numel(), _ptr(dc),
-                                              dt.code, algo, seq, s))
+                # GPU-resident rcounts / displs: the kernel reads them
+                dcnt, ddsp = _dev_vec(st, counts), _dev_vec(st, displs)
+                chk(lib.mcrdl_all_gatherv_dev(c, _ptr(i), i.numel(), _ptr(o), o.numel(),
+                                              _ptr(dcnt), _ptr(ddsp), dt.code, algo, seq, s))
             else:
                 chk(lib.mcrdl_all_gatherv(c, _ptr(i), _ptr(o), _lib.i64_array(counts),
                                           _lib.i64_array(displs), dt.code, algo, seq, s))
@@ -811,9 +811,17 @@ class NvlBackendInstance:
                 n = req.input.count
                 counts, displs = [n] * p, [r * n for r in range(p)]
             else:
-                counts, displs = _host_list(req.rcounts), _host_list(req.rdispls)
-            chk(lib.mcrdl_gatherv(c, _ptr(i), _ptr(o), _lib.i64_array(counts),
-                                  _lib.i64_array(displs), req.root, dt.code, algo, seq, s))
+                counts, displs = req.rcounts, req.rdispls
+            if _is_dev(counts) or _is_dev(displs):
+                # GPU-resident rcounts / displs: no D2H sync, the kernel reads them
+                dcnt, ddsp = _dev_vec(st, counts), _dev_vec(st, displs)
+                chk(lib.mcrdl_gatherv_dev(c, _ptr(i), i.numel(), _ptr(o),
+                                          o.numel() if o is not None else 0, _ptr(dcnt),
+                                          _ptr(ddsp), req.root, dt.code, algo, seq, s))
+            else:
+                chk(lib.mcrdl_gatherv(c, _ptr(i), _ptr(o), _lib.i64_array(_host_list(counts)),
+                                      _lib.i64_array(_host_list(displs)), req.root, dt.code,
+                                      algo, seq, s))
             return
 
         if kind in (CommOpKind.scatter, CommOpKind.scatterv):
@@ -895,6 +903,16 @@ def _host_list(x) -> list:
     if _is_dev(x):
         return [int(v) for v in x.tolist()]
     return [int(v) for v in x]
+
+
+def _dev_vec(st: _Staging, v):
+    """int64 device vector of counts (a host list is uploaded)."""
+    if _is_dev(v):
+        t = v.to(device=st.device, dtype=torch.int64).reshape(-1).contiguous()
+    else:
+        t = torch.tensor([int(x) for x in v], dtype=torch.int64).to(st.device)
+    st.keep.append(t)
+    return t
 
 
 def _dev_counts(st: _Staging, sc, sd, rc, rd):

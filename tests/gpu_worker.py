@@ -436,6 +436,25 @@ def sc_gathers(cx: Ctx):
                 if r == root:
                     cx.check(f"gatherv/{dtype.name}/{count}/root{root}", from_dev(o, dtype),
                              seqref.gatherv(ins, root, counts, displs)[root])
+            # GPU-resident rcounts / displs (mcrdl_all_gatherv_dev / mcrdl_gatherv_dev),
+            # segments packed in reverse rank order (displs not ascending)
+            gdispls, off = [0] * p, 0
+            for q in reversed(range(p)):
+                gdispls[q] = off
+                off += counts[q]
+            dcnt = torch.tensor(counts, dtype=torch.int64, device=cx.dev)
+            ddsp = torch.tensor(gdispls, dtype=torch.int64, device=cx.dev)
+            o = torch.zeros(off, dtype=i.dtype, device=cx.dev)
+            cx.rt.all_gatherv(cx.b, Buffer(o), Buffer(i), dcnt, ddsp)
+            cx.check(f"allgatherv_dev/{dtype.name}/{count}", from_dev(o, dtype),
+                     seqref.all_gatherv(ins, counts, gdispls)[r])
+            for root in (0, p - 1):
+                o = torch.zeros(off, dtype=i.dtype, device=cx.dev) if r == root else None
+                cx.rt.gatherv(cx.b, Buffer(o) if o is not None else None, Buffer(i), root, dcnt,
+                              ddsp)
+                if r == root:
+                    cx.check(f"gatherv_dev/{dtype.name}/{count}/root{root}", from_dev(o, dtype),
+                             seqref.gatherv(ins, root, counts, gdispls)[root])
         n = 333
         ins = [values(dtype, n, "ag", dtype.name, q) for q in range(p)]
         i = to_dev(ins[r], dtype, cx.dev)
