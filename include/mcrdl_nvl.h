@@ -79,7 +79,8 @@ typedef enum {
   MCRDL_ALGO_ONE_SHOT = 1,     /* all_reduce: push to all, local ascending fold   */
   MCRDL_ALGO_TWO_SHOT = 2,     /* all_reduce: RS by push + fold, AG by push      */
   MCRDL_ALGO_NVLS = 3,         /* all_reduce / bcast through NVSwitch multicast  */
-  MCRDL_ALGO_DIRECT_WRITE = 4  /* a2a(v), allgatherv, gatherv, bcast: push      */
+  MCRDL_ALGO_DIRECT_WRITE = 4, /* a2a(v), allgatherv, gatherv, bcast: push      */
+  MCRDL_ALGO_CHAIN = 5         /* bcast: pipelined chain root -> root+1 -> ...   */
 } mcrdl_algo_t;
 
 /* Payload codec flag, OR-ed into the `algo` argument of the movement

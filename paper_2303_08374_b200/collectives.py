@@ -41,7 +41,7 @@ ALGORITHMS: Dict[CommOpKind, Tuple[str, ...]] = {
     CommOpKind.all_reduce: _AR,
     CommOpKind.reduce: ("auto", "one_shot", "two_shot"),
     CommOpKind.reduce_scatter: ("auto", "two_shot"),
-    CommOpKind.bcast: ("auto", "direct_write", "nvls"),
+    CommOpKind.bcast: ("auto", "direct_write", "nvls", "chain"),
     CommOpKind.all_gather: _MOVE,
     CommOpKind.all_gatherv: _MOVE,
     CommOpKind.gather: _MOVE,
@@ -73,7 +73,8 @@ ALIASES: Dict[str, str] = {
 }
 
 # Native algorithm codes (include/mcrdl_nvl.h mcrdl_algo_t).
-ALGO_CODES = {"auto": 0, "one_shot": 1, "two_shot": 2, "nvls": 3, "direct_write": 4, "direct": 0}
+ALGO_CODES = {"auto": 0, "one_shot": 1, "two_shot": 2, "nvls": 3, "direct_write": 4, "chain": 5,
+              "direct": 0}
 
 
 def canonical(kind: CommOpKind, name: str) -> str:

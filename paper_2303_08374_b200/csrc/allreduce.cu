@@ -778,6 +778,146 @@ mcrdl_status_t launch_bcast_nvls(mcrdl_comm* c, uint8_t* buf, int64_t nbytes, in
   return MCRDL_OK;
 }
 
+// ------------------------------------------------------------ chain bcast
+// Large bcast as a pipelined chain root -> root+1 -> ... -> root+p-1: chunk j
+// is pushed into the next rank's workspace as soon as it landed in this
+// rank's, so every link carries S once and the root's egress is S (direct
+// write pushes (p-1)·S from the root; NVLS is bound by one GPU's multicast
+// stores). Each rank: NVLink ingress S + egress S, HBM ws -> buf copy fused
+// with the forward (one load, two stores).
+// Workspace reuse: every CTA first exchanges a start flag with EVERY peer, so
+// finishing op e proves each peer started op e (the all-pairs guarantee the
+// exchange engine relies on, §7 "Why bcast keeps an all-pairs handshake").
+__device__ __forceinline__ void copy2(uint8_t* d1, uint8_t* d2, const uint8_t* src, int64_t n) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  int64_t done = 0;
+  if (((uintptr_t(d1) | uintptr_t(d2) | uintptr_t(src)) & 15) == 0) {
+    const int64_t np = n >> 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* a4 = reinterpret_cast<uint4*>(d1);
+    uint4* b4 = reinterpret_cast<uint4*>(d2);
+    constexpr int U = 4;
+    int64_t i = tid;
+    for (; i + (U - 1) * nt < np; i += U * nt) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldcg(s4 + i + u * nt);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a4[i + u * nt] = v[u];
+        b4[i + u * nt] = v[u];
+      }
+    }
+    for (; i < np; i += nt) {
+      const uint4 v = __ldcg(s4 + i);
+      a4[i] = v;
+      b4[i] = v;
+    }
+    done = np << 4;
+  }
+  for (int64_t i = done + tid; i < n; i += nt) {
+    const uint8_t v = src[i];
+    d1[i] = v;
+    d2[i] = v;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_bcast_chain(DevComm c, uint8_t* buf, int64_t nb, int root, int64_t chunk, uint32_t sig) {
+  const uint32_t epoch = epoch_enter(c);
+  __shared__ SComm S;
+  __shared__ int s_err;
+  const int par = epoch & 1, rank = c.rank, world = c.world, tid = threadIdx.x;
+  const int b = blockIdx.x;
+  const int pos = (rank - root + world) % world;
+  const int pred = (rank - 1 + world) % world, succ = (rank + 1) % world;
+  const bool last = pos == world - 1;
+  const int64_t hoff = int64_t(par) * c.half_bytes;
+  if (tid == 0) s_err = 0;
+  stage_comm(c, S);
+  __syncthreads();
+  // all-pairs start handshake (per CTA)
+  if (tid < world && tid != rank) {
+    publish(&S.pad[tid]->ack[par][b][rank], make_flag(epoch, sig, 1));
+    const int e = wait_flag(&S.pad[rank]->ack[par][b][tid], S.pad[rank], c.timeout_ns, c.err,
+                            epoch, sig, 1);
+    if (e) atomicCAS(&s_err, 0, e);
+  }
+  __syncthreads();
+  if (s_err) {
+    if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+    epoch_exit(c, epoch);
+    return;
+  }
+  uint8_t* my_ws = S.ws[rank] + hoff;
+  uint8_t* succ_ws = S.ws[succ] + hoff;
+  const int64_t nch = (nb + chunk - 1) / chunk;
+  uint32_t step = 0;
+  for (int64_t j = b; j < nch; j += gridDim.x) {
+    const int64_t lo = j * chunk, len = min(chunk, nb - lo);
+    ++step;
+    if (pos == 0) {
+      block_copy<4>(succ_ws + lo, buf + lo, len);
+    } else {
+      if (tid == 0) {
+        const int e = wait_flag(&S.pad[rank]->flag[par][b][pred], S.pad[rank], c.timeout_ns,
+                                c.err, epoch, sig, step);
+        if (e) s_err = e;
+      }
+      __syncthreads();
+      if (s_err) {
+        if (tid == 0) raise_error(S.pad, world, c.err, s_err, epoch);
+        break;
+      }
+      if (last)
+        block_copy<4>(buf + lo, my_ws + lo, len);
+      else
+        copy2(succ_ws + lo, buf + lo, my_ws + lo, len);
+    }
+    if (!last) {
+      __syncthreads();
+      if (tid == 0) publish(&S.pad[succ]->flag[par][b][rank], make_flag(epoch, sig, step));
+    }
+  }
+  epoch_exit(c, epoch);
+}
+
+mcrdl_status_t launch_bcast_chain(mcrdl_comm* c, uint8_t* buf, int64_t nbytes, int root,
+                                  int dtype, uint64_t count, uint64_t seq, cudaStream_t stream) {
+  // 128 CTAs x 128 KiB chunks (profiles/r2_bcast_chain_ab.csv, p = 4: 1 GiB
+  // 644 GB/s, 256 MiB 537; 256 KiB chunks deepen the pipeline fill, 64 KiB
+  // ones cost flag round trips at 1 GiB). Knobs: every rank must agree
+  // (folded into the flag signature).
+  static const int64_t ch_ctas = env_int("MCRDL_BCAST_CHAIN_CTAS", 128);
+  static const int64_t ch_kb = env_int("MCRDL_BCAST_CHAIN_KB", 128);
+  const int64_t chunk = std::max<int64_t>(16, ch_kb) << 10;
+  const int64_t room = c->dc.half_bytes / 256 * 256;
+  int64_t done = 0;
+  int sub = 0;
+  do {
+    const int64_t nb = std::min(nbytes - done, room);
+    mcrdl_status_t st = begin_op(c, stream);
+    if (st != MCRDL_OK) return st;
+    int64_t g = (nb + chunk - 1) / chunk;
+    g = std::max<int64_t>(1, std::min<int64_t>(g, std::min<int64_t>(ch_ctas, kMaxBlocks)));
+    g = std::min<int64_t>(g, 2 * c->num_sms);
+    // <= 4095 chunks per CTA (12-bit flag steps)
+    int64_t ch = chunk;
+    while ((nb + ch * g - 1) / (ch * g) > 4095) ch *= 2;
+    const uint32_t sig = mix32(mix32(mix32(op_sig(kKindBcast, dtype, sub, root, count, seq),
+                                           uint64_t(MCRDL_ALGO_CHAIN)),
+                                     uint64_t(ch)),
+                               uint64_t(g)) &
+                         ~kSigCodecBit;
+    k_bcast_chain<<<int(g), kThreads, 0, stream>>>(c->dc, buf + done, nb, root, ch, sig);
+    count_launch();
+    MCRDL_CUDA_CHECK(cudaGetLastError());
+    done += nb;
+    ++sub;
+  } while (done < nbytes);
+  return MCRDL_OK;
+}
+
 // ------------------------------------------------------------- fused (K9)
 // Members laid out back to back in a virtual packed buffer (element offsets
 // d_off[m], 16-byte aligned). One-shot protocol over the packed index space:
@@ -1163,7 +1303,7 @@ static mcrdl_status_t ar_typed(mcrdl_comm* c, const T* in, T* out, int64_t n, mc
   if (algo == MCRDL_ALGO_NVLS && !(kNvlsType && OP == MCRDL_SUM && c->nvls.ok))
     algo = MCRDL_ALGO_TWO_SHOT;
   if (algo == MCRDL_ALGO_ONE_SHOT && bytes > oneshot_max) algo = MCRDL_ALGO_TWO_SHOT;
-  if (algo == MCRDL_ALGO_DIRECT_WRITE || algo == MCRDL_ALGO_AUTO) algo = MCRDL_ALGO_TWO_SHOT;
+  if (algo >= MCRDL_ALGO_DIRECT_WRITE || algo == MCRDL_ALGO_AUTO) algo = MCRDL_ALGO_TWO_SHOT;
   if (root < 0) c->last_algo[MCRDL_TUNE_ALL_REDUCE] = int(algo);
 
   // Host chunking keeps every launch inside one workspace (or NVLS) half.

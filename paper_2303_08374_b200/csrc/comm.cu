@@ -860,7 +860,7 @@ mcrdl_status_t mcrdl_comm_set_tuning(mcrdl_comm* c, int kind, int n, const uint6
     return set_error(MCRDL_ERR_VALIDATION, "tuning rows: n = %d", n);
   std::vector<std::pair<uint64_t, int>> rows;
   for (int i = 0; i < n; ++i) {
-    if (algos[i] < MCRDL_ALGO_AUTO || algos[i] > MCRDL_ALGO_DIRECT_WRITE)
+    if (algos[i] < MCRDL_ALGO_AUTO || algos[i] > MCRDL_ALGO_CHAIN)
       return set_error(MCRDL_ERR_VALIDATION, "tuning row %d: algorithm %d", i, algos[i]);
     if (i > 0 && max_bytes[i] <= max_bytes[i - 1])
       return set_error(MCRDL_ERR_VALIDATION, "tuning rows: max_bytes must strictly increase");

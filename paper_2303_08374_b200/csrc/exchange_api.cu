@@ -277,7 +277,9 @@ mcrdl_status_t mcrdl_gatherv_dev(mcrdl_comm* c, const void* in, uint64_t in_coun
                                  void* out_or_null, uint64_t out_count, const int64_t* d_rcounts,
                                  const int64_t* d_displs, int root, mcrdl_dtype_t dtype,
                                  mcrdl_algo_t algo, uint64_t seq, void* stream) {
-  if (c != nullptr && c->rank == root && out_or_null == nullptr)
+  // (an empty root output may be NULL: the device bounds check then rejects
+  // any nonzero count)
+  if (c != nullptr && c->rank == root && out_or_null == nullptr && out_count > 0)
     return set_error(MCRDL_ERR_VALIDATION, "root must supply the output buffer");
   return gather_dev(c, kDevGatherv, kKindGatherv, in, in_count, out_or_null, out_count, d_rcounts,
                     d_displs, root, dtype, algo, seq, stream);
@@ -305,6 +307,11 @@ mcrdl_status_t mcrdl_bcast(mcrdl_comm* c, void* buf, uint64_t count, mcrdl_dtype
     c->last_algo[MCRDL_TUNE_BCAST] = MCRDL_ALGO_NVLS;
     return launch_bcast_nvls(c, reinterpret_cast<uint8_t*>(buf), nb, root, int(dtype), count, seq,
                              reinterpret_cast<cudaStream_t>(stream));
+  }
+  if (algo == MCRDL_ALGO_CHAIN && !codec && c->world > 2) {
+    c->last_algo[MCRDL_TUNE_BCAST] = MCRDL_ALGO_CHAIN;
+    return launch_bcast_chain(c, reinterpret_cast<uint8_t*>(buf), nb, root, int(dtype), count, seq,
+                              reinterpret_cast<cudaStream_t>(stream));
   }
   c->last_algo[MCRDL_TUNE_BCAST] = MCRDL_ALGO_DIRECT_WRITE;
   ExchangeSpec s = empty_spec(es, op_sig(kKindBcast, dtype, 0, root, count, seq));

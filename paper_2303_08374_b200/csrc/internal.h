@@ -202,6 +202,8 @@ mcrdl_status_t launch_exchange(mcrdl_comm* comm, const ExchangeSpec& spec, int64
 constexpr int64_t kLLMaxPairBytes = 256 << 10;  // measured: tools/ll_ab.sh, profiles/ll_ab_r1_p{2,4}.log      // exchange: every pair <= this
 // Last bytes of each NVLS half: multicast flag words (bcast), zeroed at init.
 constexpr int64_t kNvlsFlagBytes = 64 << 10;
+mcrdl_status_t launch_bcast_chain(mcrdl_comm* c, uint8_t* buf, int64_t nbytes, int root,
+                                  int dtype, uint64_t count, uint64_t seq, cudaStream_t stream);
 mcrdl_status_t launch_bcast_nvls(mcrdl_comm* c, uint8_t* buf, int64_t nbytes, int root, int dtype,
                                  uint64_t count, uint64_t seq, cudaStream_t stream);
 // all_reduce one-shot message <= this takes LL lines; above, the bulk one-shot.

@@ -498,6 +498,29 @@ def sc_bcast_scatter(cx: Ctx):
             cx.rt.bcast(cx.b, Buffer(t), 0)
             cx.check(f"bcast/{algo}/misaligned", from_dev(t, DType.u8), ins[0])
         inst.policy = AlgorithmPolicy()
+    # pipelined chain bcast (p >= 3): partial chunks, odd sizes, a buffer
+    # misaligned on one rank, and (on the 8 MiB-workspace backend) messages
+    # spanning several launches
+    if p > 2:
+        for be, cases in ((cx.b, ((DType.u8, 1), (DType.u8, 100003), (DType.f32, (3 << 20) + 7),
+                                  (DType.bf16, 5 << 20))),
+                          ("bsmall", ((DType.f32, (5 << 20) + 3), (DType.u8, 9 << 20)))):
+            binst = cx.rt._instance(be)
+            binst.policy = AlgorithmPolicy({CommOpKind.bcast: "chain"})
+            for dtype, n in cases:
+                for root in (0, p - 1, p // 2):
+                    ins = [values(dtype, n, "bcch", be, dtype.name, n, root, q) for q in range(p)]
+                    t = to_dev(ins[r], dtype, cx.dev)
+                    cx.rt.bcast(be, Buffer(t), root)
+                    cx.check(f"bcast/chain/{be}/{dtype.name}/{n}/root{root}", from_dev(t, dtype),
+                             ins[root])
+            n = (2 << 20) + 5
+            ins = [values(DType.u8, n, "bcchmis", be, q) for q in range(p)]
+            base = to_dev(np.concatenate([np.zeros(1, np.uint8), ins[r]]), DType.u8, cx.dev)
+            t = base[1:] if r == 1 else base[1:].clone()
+            cx.rt.bcast(be, Buffer(t), 0)
+            cx.check(f"bcast/chain/{be}/misaligned", from_dev(t, DType.u8), ins[0])
+            binst.policy = AlgorithmPolicy()
     for root in range(p):
         m = 777
         src = values(DType.f32, p * m, "sc", root)
@@ -1632,6 +1655,8 @@ def run_rank(rank: int, world: int, device: int, report: str, names, shared=None
             cfgs += [BackendConfig(f"inj{k}", workspace_bytes=4 << 20) for k in range(5)]
         if "all_to_allv" in names:
             cfgs.append(BackendConfig("small", workspace_bytes=16 << 20))
+        if "bcast_scatter" in names:
+            cfgs.append(BackendConfig("bsmall", workspace_bytes=8 << 20))
         if "p2p" in names:
             cfgs.append(BackendConfig("lenm", workspace_bytes=8 << 20))
         if "codec" in names:
