@@ -779,7 +779,9 @@ mcrdl_status_t launch_bcast_nvls(mcrdl_comm* c, uint8_t* buf, int64_t nbytes, in
 }
 
 // ------------------------------------------------------------ chain bcast
-// Large bcast as a pipelined chain root -> root+1 -> ... -> root+p-1: chunk j
+// Large bcast as a pipelined chain root -> root+1 -> ... -> root+p-1 (at p = 2
+// just root -> peer, still ahead of the exchange push: 128 CTAs, no
+// receiver role, the copy-out fused per chunk): chunk j
 // is pushed into the next rank's workspace as soon as it landed in this
 // rank's, so every link carries S once and the root's egress is S (direct
 // write pushes (p-1)·S from the root; NVLS is bound by one GPU's multicast

@@ -308,7 +308,7 @@ mcrdl_status_t mcrdl_bcast(mcrdl_comm* c, void* buf, uint64_t count, mcrdl_dtype
     return launch_bcast_nvls(c, reinterpret_cast<uint8_t*>(buf), nb, root, int(dtype), count, seq,
                              reinterpret_cast<cudaStream_t>(stream));
   }
-  if (algo == MCRDL_ALGO_CHAIN && !codec && c->world > 2) {
+  if (algo == MCRDL_ALGO_CHAIN && !codec) {
     c->last_algo[MCRDL_TUNE_BCAST] = MCRDL_ALGO_CHAIN;
     return launch_bcast_chain(c, reinterpret_cast<uint8_t*>(buf), nb, root, int(dtype), count, seq,
                               reinterpret_cast<cudaStream_t>(stream));

@@ -498,10 +498,10 @@ def sc_bcast_scatter(cx: Ctx):
             cx.rt.bcast(cx.b, Buffer(t), 0)
             cx.check(f"bcast/{algo}/misaligned", from_dev(t, DType.u8), ins[0])
         inst.policy = AlgorithmPolicy()
-    # pipelined chain bcast (p >= 3): partial chunks, odd sizes, a buffer
-    # misaligned on one rank, and (on the 8 MiB-workspace backend) messages
-    # spanning several launches
-    if p > 2:
+    # pipelined chain bcast: partial chunks, odd sizes, a buffer misaligned on
+    # one rank, and (on the 8 MiB-workspace backend) messages spanning several
+    # launches
+    if p > 1:
         for be, cases in ((cx.b, ((DType.u8, 1), (DType.u8, 100003), (DType.f32, (3 << 20) + 7),
                                   (DType.bf16, 5 << 20))),
                           ("bsmall", ((DType.f32, (5 << 20) + 3), (DType.u8, 9 << 20)))):
