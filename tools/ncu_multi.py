@@ -37,6 +37,7 @@ OPS = [
     ("a2a_64m", "all_to_all_single", 64 * MIB, "auto"),
     ("a2a_ll_64k", "all_to_all_single", 64 << 10, "auto"),
     ("bcast_nvls_64m", "bcast", 64 * MIB, "nvls"),
+    ("bcast_chain_256m", "bcast", 256 * MIB, "chain"),
 ]
 
 
