@@ -1490,7 +1490,8 @@ def sc_pool(cx: Ctx):
 def sc_smoke(cx: Ctx):
     """One small invocation of each hot-path family (smoke()): LL, one-shot
     and two-shot all_reduce (explicit algorithms: at p = 1 too they run their
-    real kernels), all_to_allv with host and with device-resident counts."""
+    real kernels), all_to_allv with host and with device-resident counts, and
+    (p > 1) the chain bcast and all_gatherv with device-resident counts."""
     p, r = cx.p, cx.r
     inst = cx.rt._instance(cx.b)
     for algo, n in (("one_shot", 1000), ("one_shot", 70001), ("two_shot", 70001)):
@@ -1502,6 +1503,24 @@ def sc_smoke(cx: Ctx):
     inst.policy = AlgorithmPolicy()
     sc = counts_matrix(p, 5000, "smoke-a2av")
     _a2av_case(cx, "smoke/all_to_allv", DType.bf16, sc)
+    if p > 1:
+        # pipelined chain bcast and all_gatherv with GPU-resident counts
+        n = 300007
+        ins = [values(DType.u8, n, "smoke-chain", q) for q in range(p)]
+        t = to_dev(ins[r], DType.u8, cx.dev)
+        inst.policy = AlgorithmPolicy({CommOpKind.bcast: "chain"})
+        cx.rt.bcast(cx.b, Buffer(t), p - 1)
+        inst.policy = AlgorithmPolicy()
+        cx.check("smoke/bcast/chain", from_dev(t, DType.u8), ins[p - 1])
+        counts = [1000 + 37 * q for q in range(p)]
+        displs = packed(counts)
+        ins = [values(DType.i64, counts[q], "smoke-agv", q) for q in range(p)]
+        o = torch.zeros(sum(counts), dtype=torch.int64, device=cx.dev)
+        cx.rt.all_gatherv(cx.b, Buffer(o), Buffer(to_dev(ins[r], DType.i64, cx.dev)),
+                          torch.tensor(counts, dtype=torch.int64, device=cx.dev),
+                          torch.tensor(displs, dtype=torch.int64, device=cx.dev))
+        cx.check("smoke/all_gatherv_dev", from_dev(o, DType.i64),
+                 seqref.all_gatherv(ins, counts, displs)[r])
 
 
 def sc_golden(cx: Ctx):
