@@ -94,3 +94,16 @@ def test_build_script_targets_sm100a():
 
     assert "arch=compute_100a,code=sm_100a" in " ".join(build.ARCH)
     assert "-lineinfo" in build.FLAGS
+
+
+def test_algorithm_codes_match_the_header():
+    """collectives.ALGO_CODES (what the tuning table's algorithm names become
+    in mcrdl_comm_set_tuning / the algo argument) equals mcrdl_algo_t."""
+    from paper_2303_08374_b200.collectives import ALGO_CODES
+
+    text = HEADER.read_text()
+    enum = {m.group(1).lower(): int(m.group(2))
+            for m in re.finditer(r"MCRDL_ALGO_([A-Z_]+)\s*=\s*(\d+)", text)}
+    assert enum, "mcrdl_algo_t not found"
+    for name, code in enum.items():
+        assert ALGO_CODES[name] == code, name

@@ -187,3 +187,21 @@ def test_runtime_algorithm_table_default_and_override(tmp_path, monkeypatch):
     assert rt.algorithm_table is rt.tuning_table
     monkeypatch.setenv("MCRDL_ALGO_TABLE", "off")
     assert Runtime(0, 1).algorithm_table is None
+
+
+def test_shipped_table_bcast_rows_end_on_chain():
+    """bcast: push for small messages, then (p = 4) NVLS, then the pipelined
+    chain for large ones; every shipped algorithm name is one the policy
+    layer accepts for its op."""
+    from paper_2303_08374_b200 import dispatch
+    from paper_2303_08374_b200.collectives import ALGORITHMS
+    from paper_2303_08374_b200.core import CommOpKind
+
+    t = dispatch.default_algorithm_table()
+    for w in (2, 4):
+        rows = dispatch.algorithm_rows(t, CommOpKind.bcast, w, "nvl")
+        assert rows[0][1] == "direct_write" and rows[-1][1] == "chain", rows
+        assert all(a in ALGORITHMS[CommOpKind.bcast] for _, a in rows)
+    for kind in (CommOpKind.all_reduce, CommOpKind.all_to_allv, CommOpKind.all_gatherv):
+        for w in (2, 4):
+            assert all(a in ALGORITHMS[kind] for _, a in dispatch.algorithm_rows(t, kind, w, "nvl"))
