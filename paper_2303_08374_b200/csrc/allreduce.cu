@@ -900,12 +900,9 @@ mcrdl_status_t launch_bcast_chain(mcrdl_comm* c, uint8_t* buf, int64_t nbytes, i
     const int64_t nb = std::min(nbytes - done, room);
     mcrdl_status_t st = begin_op(c, stream);
     if (st != MCRDL_OK) return st;
-    int64_t g = (nb + chunk - 1) / chunk;
-    g = std::max<int64_t>(1, std::min<int64_t>(g, std::min<int64_t>(ch_ctas, kMaxBlocks)));
-    g = std::min<int64_t>(g, 2 * c->num_sms);
-    // <= 4095 chunks per CTA (12-bit flag steps)
-    int64_t ch = chunk;
-    while ((nb + ch * g - 1) / (ch * g) > 4095) ch *= 2;
+    // CTAs and chunk (<= kMaxSteps chunks per CTA: 12-bit flag steps), geometry.h
+    const ChainGeo geo = chain_geo(nb, chunk, ch_ctas, c->num_sms, kMaxBlocks);
+    const int64_t g = geo.g, ch = geo.ch;
     const uint32_t sig = mix32(mix32(mix32(op_sig(kKindBcast, dtype, sub, root, count, seq),
                                            uint64_t(MCRDL_ALGO_CHAIN)),
                                      uint64_t(ch)),

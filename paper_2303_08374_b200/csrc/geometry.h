@@ -127,4 +127,20 @@ MCRDL_HD Span span_of(int64_t B, int64_t slot, int g, int64_t ch, int64_t t, int
   return sp;
 }
 
+// Chain bcast (k_bcast_chain): one launch of nb bytes is cut into chunks of
+// `ch` bytes; CTA b serves chunks b, b + g, ... and counts one flag step per
+// chunk, so ch doubles until no CTA needs more than kMaxSteps steps.
+struct ChainGeo {
+  int64_t g;   // CTAs
+  int64_t ch;  // chunk bytes
+};
+MCRDL_HD ChainGeo chain_geo(int64_t nb, int64_t chunk, int64_t ctas, int num_sms, int max_blocks) {
+  int64_t g = (nb + chunk - 1) / chunk;
+  g = gmax(1, gmin(g, gmin(ctas, int64_t(max_blocks))));
+  g = gmax(1, gmin(g, int64_t(2) * num_sms));
+  int64_t ch = chunk;
+  while ((nb + ch * g - 1) / (ch * g) > kMaxSteps) ch *= 2;
+  return ChainGeo{g, ch};
+}
+
 }  // namespace mcrdl

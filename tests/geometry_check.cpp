@@ -113,7 +113,31 @@ static void check_pair(int64_t B, int p) {
   ++g_cases;
 }
 
+// Chain bcast launch of nb bytes: chunks cover [0, nb) exactly once, CTA
+// shares are disjoint, flag steps fit 12 bits, CTAs fit the flag slots.
+static void check_chain(int64_t nb, int num_sms) {
+  const ChainGeo geo = chain_geo(nb, 128 << 10, 128, num_sms, kMaxBlocks);
+  if (geo.g < 1 || geo.g > kMaxBlocks || geo.g > 2 * num_sms) fail("chain CTAs", nb, geo.g, num_sms);
+  const int64_t nch = (nb + geo.ch - 1) / geo.ch;
+  int64_t covered = 0, expect = 0;
+  for (int64_t j = 0; j < nch; ++j) {  // chunk j belongs to CTA j % g, step j / g + 1
+    const int64_t lo = j * geo.ch, hi = gmin(nb, lo + geo.ch);
+    if (lo != expect || hi <= lo) fail("chain chunk gap / overlap", nb, j, lo);
+    expect = hi;
+    covered += hi - lo;
+    if (j / geo.g + 1 > 4095) fail("flag step overflow (chain)", nb, j, geo.g);
+  }
+  if (covered != nb) fail("chain bytes not covered exactly once", nb, covered, geo.ch);
+  ++g_cases;
+}
+
 int main() {
+  // chain bcast: one launch is at most a workspace half; co-located budgets too
+  for (int sms : {148, 18, 4})
+    for (int64_t nb : {int64_t(1), int64_t(4095), int64_t(128) << 10, (int64_t(128) << 10) + 1,
+                       int64_t(300007), int64_t(64) << 20, (int64_t(1) << 30) - 3, kHalf,
+                       int64_t(4) << 30})
+      check_chain(nb, sms);
   for (int p : {2, 4, 8}) {
     // cfg2: all_reduce sweep 8 B - 1 GiB, f32 and bf16 (+ odd sizes)
     for (int k = 3; k <= 30; ++k)
